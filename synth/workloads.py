@@ -1,0 +1,211 @@
+"""Synthetic workloads shaped like the paper's benchmarks (BASELINE.json `configs`).
+
+A workload is a prefix tree of shared KV segments plus a batch of decode requests:
+  * nodes  — shared prefix segments (workflow template -> role -> ...); the tree induced by
+             the consolidated query-plan DAG (PAPER.md:54 §1, :273 §3.1 example; template
+             fan-out :135 §2.2; fan-out/fan-in primitives :296-302 §3.2),
+  * requests — each hangs under one leaf node (or none) and owns a private suffix.
+Values come from `synth.gen` (counter-based, identical on CPU and GPU).  Nothing here does
+attention arithmetic.
+
+Decode-step convention (reading R4): a step appends ONE new token per request
+(K/V from `new_kv(step)`) and then attends with `q(step)`; the attended context of request
+r after step s is  path(r) nodes ++ initial suffix ++ new tokens of steps 0..s.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .gen import TensorKey, bf16_tensor
+
+
+@dataclass(frozen=True)
+class NodeSpec:
+    ident: int
+    parent: int  # -1 for a root
+    ntok: int
+
+
+@dataclass(frozen=True)
+class RequestSpec:
+    ident: int
+    leaf: int     # -1: no shared prefix
+    suffix: int   # private tokens present before the first decode step
+
+
+@dataclass
+class Workload:
+    name: str
+    layers: int
+    hq: int
+    hkv: int
+    d: int
+    nodes: list
+    requests: list
+    seed: int = 0
+    alpha_q: float = 1.0
+    notes: dict = field(default_factory=dict)
+
+    # ---- structure -------------------------------------------------------------------
+    @property
+    def g(self) -> int:
+        return self.hq // self.hkv
+
+    @property
+    def nreq(self) -> int:
+        return len(self.requests)
+
+    def node(self, ident: int) -> NodeSpec:
+        return self._nodes_by_id[ident]
+
+    def __post_init__(self):
+        self._nodes_by_id = {n.ident: n for n in self.nodes}
+        assert self.hq % self.hkv == 0
+        offs = np.zeros(len(self.requests) + 1, dtype=np.int64)
+        for i, r in enumerate(self.requests):
+            offs[i + 1] = offs[i] + r.suffix
+        self.suffix_offsets = offs
+
+    def path(self, r: int) -> list:
+        """Node ids root -> leaf for request index r."""
+        out = []
+        n = self.requests[r].leaf
+        while n != -1:
+            out.append(n)
+            n = self._nodes_by_id[n].parent
+        return out[::-1]
+
+    def context_len(self, r: int, steps: int = 1) -> int:
+        return sum(self.node(n).ntok for n in self.path(r)) + self.requests[r].suffix + steps
+
+    # ---- tensors (layout [layer][token][head][d], bf16) -------------------------------
+    def _key(self, kind: str, ident: int) -> TensorKey:
+        return TensorKey(self.seed, kind, ident)
+
+    def node_kv(self, n: int, device="cpu", layer=None):
+        nt = self.node(n).ntok
+        return self._pair("node_k", "node_v", n, nt, self.hkv, device, layer)
+
+    def suffix_kv(self, device="cpu", layer=None, request=None):
+        """Initial suffixes of all requests: [L][sum S][Hkv][d], or one request's slice."""
+        tot = int(self.suffix_offsets[-1])
+        row = self.hkv * self.d
+        if request is None:
+            return self._pair("suf_k", "suf_v", 0, tot, self.hkv, device, layer)
+        s0, s1 = int(self.suffix_offsets[request]), int(self.suffix_offsets[request + 1])
+        assert layer is not None
+        off = (layer * tot + s0) * row
+        shape = (s1 - s0, self.hkv, self.d)
+        return (bf16_tensor(self._key("suf_k", 0), shape, device, off),
+                bf16_tensor(self._key("suf_v", 0), shape, device, off))
+
+    def q(self, step: int, device="cpu", layer=None, request=None):
+        """Decode queries of step `step`: [L][R][Hq][d] (or a slice)."""
+        return self._rows("q", step, self.hq, device, layer, request, self.alpha_q)
+
+    def new_kv(self, step: int, device="cpu", layer=None, request=None):
+        """K/V of the token appended at step `step`: [L][R][Hkv][d] (or a slice)."""
+        return (self._rows("new_k", step, self.hkv, device, layer, request),
+                self._rows("new_v", step, self.hkv, device, layer, request))
+
+    def _pair(self, kk, kv, ident, ntok, heads, device, layer):
+        row = heads * self.d
+        if layer is None:
+            shape, off = (self.layers, ntok, heads, self.d), 0
+        else:
+            shape, off = (ntok, heads, self.d), layer * ntok * row
+        return (bf16_tensor(self._key(kk, ident), shape, device, off),
+                bf16_tensor(self._key(kv, ident), shape, device, off))
+
+    def _rows(self, kind, ident, heads, device, layer, request, alpha=1.0):
+        R = self.nreq
+        row = heads * self.d
+        if layer is None:
+            assert request is None
+            return bf16_tensor(self._key(kind, ident), (self.layers, R, heads, self.d), device,
+                               0, alpha)
+        if request is None:
+            return bf16_tensor(self._key(kind, ident), (R, heads, self.d), device,
+                               layer * R * row, alpha)
+        return bf16_tensor(self._key(kind, ident), (heads, self.d), device,
+                           (layer * R + request) * row, alpha)
+
+
+# ---------------------------------------------------------------------------------------
+# Config builders.  C0..C4 follow BASELINE.json `configs`; the small
+# parity variants keep the same structure at sizes the fp64 oracle finishes in seconds.
+# ---------------------------------------------------------------------------------------
+
+def _fanout(name, layers, hq, hkv, d, nreq, prefix, suffix, seed, **kw):
+    nodes = [NodeSpec(0, -1, prefix)] if prefix > 0 else []
+    leaf = 0 if prefix > 0 else -1
+    reqs = [RequestSpec(i, leaf, suffix) for i in range(nreq)]
+    return Workload(name, layers, hq, hkv, d, nodes, reqs, seed, **kw)
+
+
+def toy(seed=0, **kw):
+    """C0: 4 requests share a 64-token prefix, 16-token suffixes (15 + the decoded token),
+    1 head, d=64."""
+    return _fanout("toy", 1, 1, 1, 64, 4, 64, 15, seed, **kw)
+
+
+def fanout(seed=1, layers=32, nreq=256, prefix=2048, suffix=255, hq=32, hkv=8, d=128, **kw):
+    """C1: Llama-3-8B GQA; `nreq` requests fanned out from one template prefix.  The
+    suffix is 255 initial tokens + the decoded token = 256 attended suffix tokens."""
+    return _fanout("fanout", layers, hq, hkv, d, nreq, prefix, suffix, seed, **kw)
+
+
+def tree(seed=2, layers=32, root=4096, roles=16, role_tok=1024, per_role=64, suffix=255,
+         hq=32, hkv=8, d=128, **kw):
+    """C2: system prompt -> role prefixes -> requests (consolidated agent DAG)."""
+    nodes = [NodeSpec(0, -1, root)] + [NodeSpec(1 + i, 0, role_tok) for i in range(roles)]
+    reqs = [RequestSpec(i, 1 + i // per_role, suffix) for i in range(roles * per_role)]
+    return Workload("tree", layers, hq, hkv, d, nodes, reqs, seed, **kw)
+
+
+def analytics(seed=3, layers=32, templates=8, ctx=8192, per_template=256, suffix=255,
+              hq=32, hkv=8, d=128, **kw):
+    """C3: batch analytics; `templates` independent shared contexts (8 per GPU of 64)."""
+    nodes = [NodeSpec(i, -1, ctx) for i in range(templates)]
+    reqs = [RequestSpec(i, i // per_template, suffix) for i in range(templates * per_template)]
+    return Workload("analytics", layers, hq, hkv, d, nodes, reqs, seed, **kw)
+
+
+def ragged(seed=4, layers=2, hq=8, hkv=2, d=128, **kw):
+    """Parity stress: a depth-3 tree with partial blocks, requests without a prefix,
+    ragged suffixes (incl. 0 initial tokens), and one node shared by a single request."""
+    rng = np.random.Generator(np.random.PCG64(1000 + seed))
+    nodes = [NodeSpec(0, -1, 301), NodeSpec(1, 0, 77), NodeSpec(2, 0, 160),
+             NodeSpec(3, 1, 33), NodeSpec(4, -1, 5), NodeSpec(5, 2, 129)]
+    leaves = [0, 1, 2, 3, 3, 3, 4, 5, -1, 2, 1, 5, 3, 0, -1, 2] * 3
+    reqs = []
+    for i, lf in enumerate(leaves):
+        s = int(rng.integers(0, 300)) if i % 7 else 0
+        reqs.append(RequestSpec(i, lf, s))
+    return Workload("ragged", layers, hq, hkv, d, nodes, reqs, seed, **kw)
+
+
+def ragged_suffix(seed=5, layers=2, nreq=96, prefix=1024, lo=128, hi=1024, hq=32, hkv=8,
+                  d=128, **kw):
+    """C1 variant with S_r ~ U[lo, hi] (the output-length range of PAPER.md:685 §4.5)."""
+    rng = np.random.Generator(np.random.PCG64(2000 + seed))
+    nodes = [NodeSpec(0, -1, prefix)]
+    reqs = [RequestSpec(i, 0, int(rng.integers(lo, hi + 1)) - 1) for i in range(nreq)]
+    return Workload("ragged_suffix", layers, hq, hkv, d, nodes, reqs, seed, **kw)
+
+
+CONFIGS = {
+    "toy": toy,
+    "fanout": fanout,
+    "tree": tree,
+    "analytics": analytics,
+    "ragged": ragged,
+    "ragged_suffix": ragged_suffix,
+}
+
+
+def make_config(name: str, **kw) -> Workload:
+    return CONFIGS[name](**kw)

@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py -- shared-prefix decode attention on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], "C1"): Llama-3-8B GQA (32 q / 8 kv heads, d=128, bf16
+KV in 16-token paged blocks), 256 requests fanned out from one 2,048-token workflow-template
+prefix, 256-token private suffixes, 32 layers, one B200 per rank.  Synthetic seeded data
+(synth/), resident in HBM before the timed region.
+
+A STEP is one decode step of the whole hot path over the batch:
+  roll back last step's token (host bookkeeping) + append this step's token K/V for all 32
+  layers (K5) + plan (host, uploaded) + for each of 32 layers: K1 (tcgen05 prefix
+  attention over the shared node) and K2+K3 (paged suffix decode + LSE merge).
+queries/s = requests x layers x steps / time  (1 query = one request's decode attention at
+one layer over all its heads; SURVEY.md §8(c) reading 13).
+
+N>1 (torchrun): weak scaling -- every rank runs its own independent C1 batch (request groups
+partition across GPUs with no exchange on the attention path); time = max
+over ranks.  KV migration (K4 pack + NCCL send/recv + K4 unpack) is measured in the same run
+and reported under "migration" (N=1: same-GPU relocation through K4, no NCCL).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "shared-prefix decode attn queries/s; HBM GB/s & TC util vs peak; KV migrate GB/s"
+UNIT = "queries/s"
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+FALLBACK_BF16_TFLOPS = 1590.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", FALLBACK_HBM_GBS), d.get("bf16_tflops", FALLBACK_BF16_TFLOPS), \
+            d.get("bf16_tflops_sustained"), "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].startswith("Active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(self.rows[0][1]), "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((num(r[2]) or 0) for r in self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ oracle (CPU) legs
+def oracle_sample(wl, budget_s: float, max_requests: int = 64, layer: int = 0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the same workload:
+    requests of `layer` after one decode step, contexts gathered outside the timer."""
+    import numpy as np
+    import oracle
+    nthreads = host_cores()
+    scale = 1.0 / np.sqrt(wl.d)
+    t_total, done = 0.0, 0
+    for r in range(min(wl.nreq, max_requests)):
+        k, v = oracle.request_context(wl, r, layer, steps=1)
+        qb = oracle._bits(wl.q(0, "cpu", layer, request=r))
+        t0 = time.perf_counter()
+        oracle.attend(qb, k, v, scale, nthreads)
+        t_total += time.perf_counter() - t0
+        done += 1
+        if t_total >= budget_s:
+            break
+    return done, t_total, nthreads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle; the others exit 0 without work
+    from synth import make_config
+    wl = make_config(args.config)
+    # each step = the oracle on a bounded sample (8 requests, layer 0)
+    import numpy as np
+    import oracle
+    nthreads = host_cores()
+    scale = 1.0 / np.sqrt(wl.d)
+    ctx = []
+    for r in range(8):
+        k, v = oracle.request_context(wl, r, 0, steps=1)
+        ctx.append((oracle._bits(wl.q(0, "cpu", 0, request=r)), k, v))
+
+    def step():
+        for qb, k, v in ctx:
+            oracle.attend(qb, k, v, scale, nthreads)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = len(ctx) * args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, synth/)",
+        "config": {"workload": "C1 fanout: 256 req x 2048-token shared prefix + 256-token suffix, "
+                               "Llama-3-8B GQA 32q/8kv d128, 32 layers",
+                   "sample": "8 requests x layer 0 per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                         "sample": "8 requests of C1 at layer 0 per step (unshared fp64 attention)",
+                         "cpu_model": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="halo", choices=["halo", "reference"])
+    ap.add_argument("--config", default="fanout")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle time")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-migration", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2509_02121_b200 as halo
+    from paper_2509_02121_b200.loader import blocks_needed, load
+    from synth import make_config
+
+    rank, world, local = dist_env()
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    halo.load_library()
+
+    wl = make_config(args.config, seed=1 + 1000 * rank)
+    L, R, Hq, Hkv, D = wl.layers, wl.nreq, wl.hq, wl.hkv, wl.d
+    ld = load(wl, dev, capacity=blocks_needed(wl, steps=2, slack=4096))
+    pool, reqs = ld.pool, ld.req_ids
+    nk, nv = wl.new_kv(0, f"cuda:{dev}")            # [L][R][Hkv][D] this step's token
+    q = wl.q(0, f"cuda:{dev}")                      # [L][R][Hq][D]
+    out = torch.empty((L, R, Hq, D), device=f"cuda:{dev}")
+    lse = torch.empty((L, R, Hq), device=f"cuda:{dev}")
+    ones = [1] * R
+    pool.append(reqs, ones, nk, nv)
+    plan = pool.plan(reqs)
+    info = plan.info()
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        pool.truncate(reqs, ones)                 # stationary batch: roll back, re-append
+        pool.append(reqs, ones, nk, nv)
+        pool.plan(reqs, reuse=plan)
+        for l in range(L):
+            if evs is not None:
+                evs[l][0].record(stream)
+            plan.run_stages(l, 1, q[l], out[l], lse[l])
+            if evs is not None:
+                evs[l][1].record(stream)
+            plan.run_stages(l, 2, q[l], out[l], lse[l])
+            if evs is not None:
+                evs[l][2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)]
+           for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        t_start.record(stream)
+        for s in range(args.steps):
+            step(evs[s])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    k1_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st)
+    k2_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st)
+    if world > 1:
+        t = torch.tensor([ms, k1_ms, k2_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, k1_ms, k2_ms = t.tolist()
+    launches = args.steps * (1 + 2 * L)
+    ms_step = ms / args.steps
+    value = R * L * world * args.steps / (ms / 1e3)
+
+    hbm_peak, tc_peak, tc_sustained, peak_src = peaks()
+    k2_launch_ms = k2_ms / (args.steps * L)
+    k1_launch_ms = k1_ms / (args.steps * L)
+    k2_gbs = info["k2_bytes"] / (k2_launch_ms * 1e-3) / 1e9
+    k1_tflops = info["k1_flops"] / (k1_launch_ms * 1e-3) / 1e12 if info["k1_flops"] else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("suffix_decode_kernel", {}).get("dram_bytes_per_launch")
+
+    extra = {}
+    # ---- e2e: the public API with HOST buffers (pinned), copies inside the timed region ----
+    if not args.no_e2e and not args.profile:
+        nk_h, nv_h = nk.cpu().pin_memory(), nv.cpu().pin_memory()
+        q_h = q.cpu().pin_memory()
+        out_h = torch.empty((L, R, Hq, D), pin_memory=True)
+        e2e_steps = min(args.steps, 30)
+
+        def e2e_step():
+            pool.truncate(reqs, ones)
+            pool.append(reqs, ones, nk_h, nv_h)
+            pool.plan(reqs, reuse=plan)
+            plan.run_layers(L, q_h, out_h)
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], device=f"cuda:{dev}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = tt.item()
+        h2d = nk_h.numel() * 2 * 2 + q_h.numel() * 2
+        d2h = out_h.numel() * 4
+        extra["e2e"] = {"value": R * L * world * e2e_steps / dt, "unit": UNIT,
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "steps": e2e_steps, "how": "halo_suffix_append + halo_decode_plan + "
+                        "halo_decode_layers with pinned host buffers; wall clock after sync"}
+    # ---- migration (K4 + NCCL), measured in the same run ----
+    if not args.no_migration and not args.profile:
+        extra["migration"] = measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist)
+    # ---- CPU oracle baseline ----
+    if rank == 0 and not args.no_cpu_baseline and not args.profile:
+        n, t, cores = oracle_sample(wl, args.cpu_budget)
+        extra["cpu_baseline"] = {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                 "sample": f"{n} requests of C1 at layer 0 (unshared fp64 "
+                                           f"attention over 2304 tokens x 32 heads), "
+                                           f"{t:.1f} s", "cpu_model": cpu_model()}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator, synth/); no weights needed",
+            "config": {"workload": "C1 fanout: 256 req x 2048-token shared prefix + 256-token "
+                                   "suffix, Llama-3-8B GQA 32q/8kv d128, 32 layers, 16-token blocks",
+                       "requests_per_gpu": R, "layers": L, "prefix_tokens": wl.nodes[0].ntok,
+                       "suffix_tokens": wl.requests[0].suffix + 1,
+                       "parallelism": f"request-group sharding x{world} (no collective)",
+                       "l2": "inputs exceed L2 (8.3 GiB KV touched per step vs 126 MB L2)",
+                       "k1_tiles": info["k1_tiles"], "k2_units": info["k2_units"]},
+            "roofline": {"bound": "hbm", "kernel": "suffix_decode_kernel (K2+K3)",
+                         "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": k2_gbs / hbm_peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": info["k2_bytes"],
+                         "avg_launch_ms": k2_launch_ms, "peak_source": peak_src},
+            "prefix_roofline": {"bound": "tensor", "kernel": "prefix_attn_kernel (K1)",
+                                "achieved": k1_tflops, "peak": tc_peak, "unit": "TFLOP/s",
+                                "frac": (k1_tflops / tc_peak) if k1_tflops else None,
+                                "algorithmic_flops_per_launch": info["k1_flops"],
+                                "avg_launch_ms": k1_launch_ms, "peak_source": peak_src},
+            "step_breakdown_ms": {"k1": k1_ms / args.steps, "k2": k2_ms / args.steps,
+                                  "other": ms_step - (k1_ms + k2_ms) / args.steps},
+            "unshared_bytes_per_layer": info["unshared_bytes"],
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    plan.destroy()
+    pool.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):
+    node = ld.node_ids[0]
+    ntok = wl.nodes[0].ntok
+    nbytes = ntok * wl.layers * wl.hkv * wl.d * 2 * 2
+    if world == 1:
+        dst = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, (ntok + 15) // 16 * 3, dev)
+        for _ in range(2):
+            n = pool.clone_prefix(node, dst, -1)
+            torch.cuda.synchronize()
+            dst.release_prefix(n)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        n = pool.clone_prefix(node, dst, -1)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        dst.release_prefix(n)
+        dst.destroy()
+        return {"mode": "same-GPU relocation through K4 pack+unpack (no NCCL at N=1)",
+                "bytes": nbytes, "ms": ms, "GB/s": nbytes / ms / 1e6,
+                "hbm_bytes": 4 * nbytes, "hbm_GB/s": 4 * nbytes / ms / 1e6}
+    uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
+    obj = [uid]
+    dist.broadcast_object_list(obj, src=0)
+    pool.comm_init(obj[0], world, rank)
+    res = {}
+    for it in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        newn = None
+        if rank == 0:
+            pool.migrate_send(node, 1, 1)
+        elif rank == 1:
+            newn = pool.migrate_recv(0, -1, ntok)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{dev}")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        if newn is not None:
+            pool.release_prefix(newn)
+        res = {"mode": "rank0 -> rank1 NCCL send/recv (COPY), K4 pack/unpack pipelined",
+               "bytes": nbytes, "ms": ms.item(), "GB/s": nbytes / ms.item() / 1e6}
+    return res
+
+
+if __name__ == "__main__":
+    main()

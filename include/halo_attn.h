@@ -1,0 +1,229 @@
+/*
+ * halo_attn.h -- C ABI of the B200-native shared-prefix decode-attention library.
+ *
+ * The hot path behind Halo's KV-cache sharing (arXiv 2509.02121):
+ *   - a shared prefix cache: a prefix's K/V is computed once and reused by every later
+ *     query with that prefix (§3.3 "Prefix caching");
+ *   - the consolidated query-plan DAG makes batched requests share prompt prefixes
+ *     (PAPER.md:54 §1, :273 §3.1), which induces a TREE of shared KV segments;
+ *   - decode reuses cached key/value tensors and is memory-bound (§2.1,
+ *     :341 §3.3), with the decode batch grown to the memory limit (:341);
+ *   - KV tensors are the standardised state exchanged at operator boundaries
+ *     ("On-the-fly context exchange"); the exchange layout below is
+ *     [layer][token][kv_head][head_dim] bf16;
+ *   - cache snapshots migrate among GPUs via NVLink under scheduler control
+ *     (PAPER.md:337 §3.3, :673 §4.5);
+ *   - every optimisation is semantics-preserving: the shared-prefix result equals naive
+ *     unshared attention (§2.2 "Exact answers").
+ *
+ * Only plain C types cross this boundary.  Every `stream` argument is a cudaStream_t
+ * passed as void* (NULL = legacy default stream).  Unless stated otherwise, data
+ * pointers are DEVICE pointers of the pool's device; entries marked "host or device"
+ * accept either (host memory is staged by the library; pinned memory is fastest).
+ *
+ * Errors: every call returns a halo_status.  Host-side validation finishes before any
+ * device work is enqueued; on a non-OK status the library state is unchanged (no partial
+ * registration, no leaked blocks).  Asynchronous device faults surface as HALO_ECUDA at
+ * the next call that synchronises.  No C++ exception crosses the ABI.  The text of the
+ * last error on the calling thread is returned by halo_last_error().
+ *
+ * Threading: a pool (and its plans) is externally synchronised -- one host thread at a
+ * time.  All device work is stream-ordered on the caller's stream.
+ *
+ * Ids: node and request ids are int64, unique and never reused within a pool.
+ */
+#ifndef HALO_ATTN_H
+#define HALO_ATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HALO_ABI_VERSION 1
+#define HALO_BLOCK_TOKENS 16
+
+typedef int32_t halo_status;
+enum {
+    HALO_OK = 0,
+    HALO_EINVAL = 1,        /* bad argument (shape, id kind, null pointer, ...)        */
+    HALO_ENOMEM = 2,        /* pool out of blocks, or a device/host allocation failed   */
+    HALO_ENOENT = 3,        /* unknown node / request id                                */
+    HALO_EBUSY = 4,         /* node still referenced by children or requests            */
+    HALO_ECUDA = 5,         /* a CUDA runtime/driver call failed                        */
+    HALO_ENCCL = 6,         /* an NCCL call failed, or no communicator                  */
+    HALO_EUNSUPPORTED = 7   /* valid but not supported (e.g. compute on a host-only pool) */
+};
+
+typedef struct halo_pool_s *halo_pool;
+typedef struct halo_plan_s *halo_plan;
+
+/* Text of the last non-OK status raised on this thread ("" if none).  Owned by the
+ * library; valid until the next call on this thread. */
+const char *halo_last_error(void);
+int32_t halo_abi_version(void);
+
+/* ------------------------------------------------------------------ paged KV pool */
+/* A pool holds K and V for `num_layers` layers in fixed blocks of 16 tokens.  Device
+ * layout of each of K and V (bf16):
+ *     [layer][block][kv_head][16][head_dim]
+ * so one (block, kv_head) slab is 16*head_dim*2 bytes contiguous (4 KiB at d=128).
+ * (Block-level KV management as in vLLM, §4.1 Baselines.) */
+typedef struct {
+    int32_t device;          /* CUDA ordinal.  -1 = host-only bookkeeping: no device
+                                memory, no launches (used to test allocator/tree/plan on
+                                machines without a GPU; compute calls return
+                                HALO_EUNSUPPORTED). */
+    int32_t num_layers;      /* >= 1 */
+    int32_t num_kv_heads;    /* kv heads held by THIS pool (a shard when heads are split) */
+    int32_t num_q_heads;     /* q heads served; a multiple g of num_kv_heads; q-head h
+                                reads kv head floor(h/g) (reading R3)          */
+    int32_t head_dim;        /* 64 or 128 */
+    int32_t block_tokens;    /* must be HALO_BLOCK_TOKENS (16) */
+    int64_t capacity_blocks; /* blocks per layer */
+    void *k_storage;         /* optional caller-owned device memory for K (and V), each of
+                                >= halo_pool_storage_bytes(cfg) bytes, 256-B aligned;
+                                NULL => the library allocates (and frees) it.           */
+    void *v_storage;
+} halo_pool_config;
+
+/* Bytes of ONE of the K or V arrays for this config. */
+size_t halo_pool_storage_bytes(const halo_pool_config *cfg);
+halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out);
+/* Frees every node, request and plan resource of the pool.  Plans created on it must be
+ * destroyed first (EBUSY otherwise). */
+halo_status halo_pool_destroy(halo_pool pool);
+halo_status halo_pool_stats(halo_pool pool, int64_t *free_blocks, int64_t *used_blocks);
+/* Device base pointers of the K and V arrays (layout above).  For tests and tools. */
+halo_status halo_pool_storage(halo_pool pool, void **k, void **v);
+
+/* ------------------------------------------------------------------ prefix nodes */
+/* Register an immutable shared prefix segment of `ntok` tokens under `parent` (-1 = a
+ * root): the "shared prefix cache" entry of PAPER.md:343.  k, v (host or device):
+ * bf16 [num_layers][ntok][num_kv_heads][head_dim] (the exchange layout).  Copies the
+ * tokens into freshly allocated blocks on `stream` (tail of the last block zero-filled);
+ * the caller may reuse k/v once `stream` has passed this point.  ntok >= 1. */
+halo_status halo_prefix_register(halo_pool pool, int64_t parent, int32_t ntok,
+                                 const void *k, const void *v, void *stream,
+                                 int64_t *node_out);
+/* Release a node: EBUSY while it has children or open requests.  Its blocks return to
+ * the pool once work already enqueued on the pool's streams has passed. */
+halo_status halo_prefix_release(halo_pool pool, int64_t node);
+/* Gather a node's tokens out of the pool into k_out, v_out (device): bf16
+ * [num_layers][ntok][num_kv_heads][head_dim].  This is the K4 pack kernel. */
+halo_status halo_prefix_read(halo_pool pool, int64_t node, void *k_out, void *v_out,
+                             void *stream);
+/* Introspection: parent, token count, block count, and (if blocks_out != NULL, with room
+ * for *nblocks entries) the block ids in token order. */
+halo_status halo_node_info(halo_pool pool, int64_t node, int64_t *parent, int32_t *ntok,
+                           int32_t *nblocks, int32_t *blocks_out);
+
+/* ------------------------------------------------------------------ requests */
+/* Open a decode request under prefix node `leaf` (-1 = no shared prefix).  Its private
+ * suffix starts empty and always starts in a fresh block (reading R11). */
+halo_status halo_request_open(halo_pool pool, int64_t leaf, int64_t *req_out);
+halo_status halo_request_close(halo_pool pool, int64_t req);
+halo_status halo_request_info(halo_pool pool, int64_t req, int64_t *leaf, int32_t *suffix_len,
+                              int32_t *nblocks);
+/* Append ntok[i] >= 0 tokens to the suffix of reqs[i] (reqs and ntok are HOST arrays).
+ * k, v (host or device): bf16 [num_layers][sum(ntok)][num_kv_heads][head_dim], requests
+ * in the order given.  All-or-nothing: ENOMEM leaves every suffix unchanged.  K5. */
+halo_status halo_suffix_append(halo_pool pool, int32_t nreq, const int64_t *reqs,
+                               const int32_t *ntok, const void *k, const void *v,
+                               void *stream);
+/* Drop the last ntok[i] tokens of each suffix (host-only bookkeeping; freed blocks return
+ * to the pool after enqueued work passes).  Used to roll back tokens. */
+halo_status halo_suffix_truncate(halo_pool pool, int32_t nreq, const int64_t *reqs,
+                                 const int32_t *ntok);
+
+/* ------------------------------------------------------------------ decode step */
+typedef struct {
+    int32_t min_tensor_rows; /* a prefix node runs on the tcgen05 prefix kernel (K1) iff
+                                (#requests under it) * g >= this; others are folded into
+                                the suffix kernel as ordinary blocks.  <= 0: default 64. */
+    int32_t force_splits;    /* > 0: split every K1 node's tokens into this many ranges
+                                (tests); 0: the plan chooses (fills the 148 SMs).      */
+    int32_t max_splits;      /* cap on splits per node; <= 0: default 16                */
+    int32_t reserved;
+} halo_plan_options;
+
+/* Build (or rebuild in place, when *inout != NULL) the plan of one decode step for the
+ * batch reqs[0..nreq) (HOST array, any order).  The plan records the prefix tree of the
+ * batch in DFS order (so each node covers a contiguous request range), the K1 tile list,
+ * the K2 work list and the partial-slot map, and uploads them on `stream`.  Reuse a plan
+ * only on the stream its runs were enqueued on.  Requests with an empty context
+ * (no prefix and no suffix token) are EINVAL. */
+halo_status halo_decode_plan(halo_pool pool, int32_t nreq, const int64_t *reqs,
+                             const halo_plan_options *opt, void *stream, halo_plan *inout);
+/* Attention of layer `layer` for the planned batch:
+ *   q   : bf16 [nreq][num_q_heads][head_dim], rows in the order given to the plan
+ *   out : fp32 [nreq][num_q_heads][head_dim]   normalised attention output
+ *   lse : fp32 [nreq][num_q_heads] natural-log log-sum-exp of the scaled scores (nullable)
+ *   scale <= 0 selects 1/sqrt(head_dim).
+ * Enqueues K1 (shared prefixes, tcgen05) then K2 (private suffixes + fused LSE merge, K3).
+ * Graph-capturable. */
+halo_status halo_decode_run(halo_plan plan, int32_t layer, const void *q, float *out,
+                            float *lse, float scale, void *stream);
+/* Run only some stages of halo_decode_run (for per-kernel timing): stage_mask bit 0 = K1
+ * (prefix partials), bit 1 = K2+K3 (suffix + merge; reads the partials K1 last wrote for
+ * this plan).  halo_decode_run == stage_mask 3. */
+halo_status halo_decode_run_stages(halo_plan plan, int32_t layer, int32_t stage_mask,
+                                   const void *q, float *out, float *lse, float scale,
+                                   void *stream);
+/* All layers [0, nlayers) in one call: q (host or device) bf16 [nlayers][nreq][Hq][d],
+ * out (host or device) fp32 [nlayers][nreq][Hq][d], lse (nullable, host or device) fp32
+ * [nlayers][nreq][Hq].  Host buffers are staged through device scratch on `stream`. */
+halo_status halo_decode_layers(halo_plan plan, int32_t nlayers, const void *q, float *out,
+                               float *lse, float scale, void *stream);
+
+typedef struct {
+    int32_t nreq, num_q_heads, num_kv_heads, head_dim;
+    int32_t tensor_nodes;    /* prefix nodes on K1 */
+    int32_t folded_nodes;    /* prefix nodes folded into K2 */
+    int32_t k1_tiles;        /* K1 CTAs per layer */
+    int32_t k2_units;        /* (request, kv head) work units of K2 */
+    int32_t max_slots;       /* partial slots per request (max over requests) */
+    int32_t reserved;
+    int64_t k1_rows;         /* sum over K1 tiles of valid rows x tokens / 128 (bookkeeping) */
+    double k1_flops;         /* algorithmic FLOPs per layer: sum_nodes 4*(n_req*g)*L_n*d*Hkv */
+    double k1_bytes;         /* algorithmic bytes per layer of K1 (KV once + Q + partials) */
+    double k2_bytes;         /* algorithmic bytes per layer of K2+K3 */
+    double unshared_bytes;   /* KV bytes per layer an unshared decode would read */
+} halo_plan_info;
+halo_status halo_plan_get_info(halo_plan plan, halo_plan_info *info);
+/* Copy one of the plan's host arrays out (tests): which = 0 request DFS order (int32
+ * caller indices), 1 K1 tiles (int32 x 8 each: req_off, nrows, kv_head, tok_begin,
+ * tok_end, blk_off, slot, node_index), 2 per-request slot counts (int32), 3 K2 request
+ * order (int32), 4 per-request K2 block CSR offsets (int32, nreq+1), 5 K2 block entries
+ * (uint32: block | (ntok-1) << 27).  *n receives the element count; copies at most cap. */
+halo_status halo_plan_export(halo_plan plan, int32_t which, void *dst, int64_t cap,
+                             int64_t *n);
+halo_status halo_plan_destroy(halo_plan plan);
+
+/* ------------------------------------------------------------------ migration */
+/* NCCL point-to-point over NVLink/NVSwitch, used ONLY for KV-block migration.  The 128-B
+ * ncclUniqueId is created on one rank and broadcast by the caller (torch.distributed). */
+halo_status halo_comm_unique_id(void *id_out /* 128 bytes */);
+halo_status halo_comm_init(halo_pool pool, const void *id /* 128 bytes */, int32_t nranks,
+                           int32_t rank);
+/* Send node `node` (all layers, the pool's kv heads) to `dst_rank`: K4 pack into chunk
+ * buffers pipelined with ncclSend on an internal side stream ordered after `stream`; on
+ * return `stream` is ordered after the last send.  mode 0 = MOVE (node released after
+ * the transfer; EBUSY if referenced), 1 = COPY.  Both peers must call concurrently. */
+halo_status halo_migrate_send(halo_pool pool, int64_t node, int32_t dst_rank, int32_t mode,
+                              void *stream);
+/* Receive a node of `ntok` tokens from `src_rank` into fresh blocks and register it under
+ * `parent` (-1 = root).  ncclRecv pipelined with the K4 unpack kernel. */
+halo_status halo_migrate_recv(halo_pool pool, int32_t src_rank, int64_t parent, int32_t ntok,
+                              void *stream, int64_t *node_out);
+/* Same-device relocation: pack `node` of `src` and unpack it into `dst` (which may be the
+ * same pool) under `parent_dst`, through the same chunked K4 path as a migration. */
+halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_t parent_dst,
+                              void *stream, int64_t *node_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALO_ATTN_H */

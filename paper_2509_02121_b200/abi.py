@@ -1,0 +1,311 @@
+"""ctypes binding of include/halo_attn.h (same names as the C ABI, Pythonic wrappers).
+
+Marshalling only: tensors are passed as raw pointers, streams as cudaStream_t handles.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libhalo_attn.so")
+
+STATUS = {0: "HALO_OK", 1: "HALO_EINVAL", 2: "HALO_ENOMEM", 3: "HALO_ENOENT", 4: "HALO_EBUSY",
+          5: "HALO_ECUDA", 6: "HALO_ENCCL", 7: "HALO_EUNSUPPORTED"}
+
+# Every symbol include/halo_attn.h declares, with its ctypes signature.
+_i32, _i64, _p, _f = C.c_int32, C.c_int64, C.c_void_p, C.c_float
+_pi64, _pi32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+
+
+class PoolConfig(C.Structure):
+    _fields_ = [("device", _i32), ("num_layers", _i32), ("num_kv_heads", _i32),
+                ("num_q_heads", _i32), ("head_dim", _i32), ("block_tokens", _i32),
+                ("capacity_blocks", _i64), ("k_storage", _p), ("v_storage", _p)]
+
+
+class PlanOptions(C.Structure):
+    _fields_ = [("min_tensor_rows", _i32), ("force_splits", _i32), ("max_splits", _i32),
+                ("reserved", _i32)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("nreq", _i32), ("num_q_heads", _i32), ("num_kv_heads", _i32), ("head_dim", _i32),
+                ("tensor_nodes", _i32), ("folded_nodes", _i32), ("k1_tiles", _i32),
+                ("k2_units", _i32), ("max_slots", _i32), ("reserved", _i32), ("k1_rows", _i64),
+                ("k1_flops", C.c_double), ("k1_bytes", C.c_double), ("k2_bytes", C.c_double),
+                ("unshared_bytes", C.c_double)]
+
+
+SIGNATURES = {
+    "halo_last_error": (C.c_char_p, []),
+    "halo_abi_version": (_i32, []),
+    "halo_pool_storage_bytes": (C.c_size_t, [C.POINTER(PoolConfig)]),
+    "halo_pool_create": (_i32, [C.POINTER(PoolConfig), C.POINTER(_p)]),
+    "halo_pool_destroy": (_i32, [_p]),
+    "halo_pool_stats": (_i32, [_p, _pi64, _pi64]),
+    "halo_pool_storage": (_i32, [_p, C.POINTER(_p), C.POINTER(_p)]),
+    "halo_prefix_register": (_i32, [_p, _i64, _i32, _p, _p, _p, _pi64]),
+    "halo_prefix_release": (_i32, [_p, _i64]),
+    "halo_prefix_read": (_i32, [_p, _i64, _p, _p, _p]),
+    "halo_node_info": (_i32, [_p, _i64, _pi64, _pi32, _pi32, _pi32]),
+    "halo_request_open": (_i32, [_p, _i64, _pi64]),
+    "halo_request_close": (_i32, [_p, _i64]),
+    "halo_request_info": (_i32, [_p, _i64, _pi64, _pi32, _pi32]),
+    "halo_suffix_append": (_i32, [_p, _i32, _pi64, _pi32, _p, _p, _p]),
+    "halo_suffix_truncate": (_i32, [_p, _i32, _pi64, _pi32]),
+    "halo_decode_plan": (_i32, [_p, _i32, _pi64, C.POINTER(PlanOptions), _p, C.POINTER(_p)]),
+    "halo_decode_run": (_i32, [_p, _i32, _p, _p, _p, _f, _p]),
+    "halo_decode_run_stages": (_i32, [_p, _i32, _i32, _p, _p, _p, _f, _p]),
+    "halo_decode_layers": (_i32, [_p, _i32, _p, _p, _p, _f, _p]),
+    "halo_plan_get_info": (_i32, [_p, C.POINTER(PlanInfo)]),
+    "halo_plan_export": (_i32, [_p, _i32, _p, _i64, _pi64]),
+    "halo_plan_destroy": (_i32, [_p]),
+    "halo_comm_unique_id": (_i32, [_p]),
+    "halo_comm_init": (_i32, [_p, _p, _i32, _i32]),
+    "halo_migrate_send": (_i32, [_p, _i64, _i32, _i32, _p]),
+    "halo_migrate_recv": (_i32, [_p, _i32, _i64, _i32, _p, _pi64]),
+    "halo_prefix_clone": (_i32, [_p, _i64, _p, _i64, _p, _pi64]),
+}
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libhalo_attn.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: build it with "
+                              "`python -m paper_2509_02121_b200.build` (no CPU fallback exists)")
+        lib = C.CDLL(_LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class HaloError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{fn}: {self.name}: {msg}")
+
+
+def _check(fn: str, st: int):
+    if st != 0:
+        msg = load_library().halo_last_error().decode(errors="replace")
+        raise HaloError(st, fn, msg)
+
+
+def _call(fn: str, *args):
+    _check(fn, getattr(load_library(), fn)(*args))
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        assert t.is_contiguous(), "tensors crossing the ABI must be contiguous"
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    return int(t)
+
+
+def _stream(stream, device: int):
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    if device < 0:
+        return None
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _i64_array(xs):
+    a = (C.c_int64 * len(xs))(*[int(x) for x in xs])
+    return a
+
+
+def _i32_array(xs):
+    return (C.c_int32 * len(xs))(*[int(x) for x in xs])
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _call("halo_comm_unique_id", buf)
+    return buf.raw
+
+
+class Pool:
+    """A paged bf16 KV pool [layer][block][kv_head][16][d] (halo_pool_create)."""
+
+    def __init__(self, num_layers: int, num_kv_heads: int, num_q_heads: int, head_dim: int,
+                 capacity_blocks: int, device: int = 0, k_storage=None, v_storage=None):
+        self.cfg = PoolConfig(device, num_layers, num_kv_heads, num_q_heads, head_dim, 16,
+                              capacity_blocks, _ptr(k_storage), _ptr(v_storage))
+        self.device = device
+        self._keep = (k_storage, v_storage)
+        h = C.c_void_p()
+        _call("halo_pool_create", C.byref(self.cfg), C.byref(h))
+        self.handle = h
+
+    @property
+    def layers(self):
+        return self.cfg.num_layers
+
+    @property
+    def hkv(self):
+        return self.cfg.num_kv_heads
+
+    @property
+    def hq(self):
+        return self.cfg.num_q_heads
+
+    @property
+    def d(self):
+        return self.cfg.head_dim
+
+    def storage_bytes(self) -> int:
+        return load_library().halo_pool_storage_bytes(C.byref(self.cfg))
+
+    def destroy(self):
+        if self.handle:
+            _call("halo_pool_destroy", self.handle)
+            self.handle = None
+
+    def stats(self):
+        f, u = C.c_int64(), C.c_int64()
+        _call("halo_pool_stats", self.handle, C.byref(f), C.byref(u))
+        return f.value, u.value
+
+    def storage(self):
+        k, v = C.c_void_p(), C.c_void_p()
+        _call("halo_pool_storage", self.handle, C.byref(k), C.byref(v))
+        return k.value, v.value
+
+    def _s(self, stream):
+        return _stream(stream, self.device)
+
+    def register_prefix(self, parent: int, ntok: int, k=None, v=None, stream=None) -> int:
+        out = C.c_int64()
+        _call("halo_prefix_register", self.handle, parent, ntok, _ptr(k), _ptr(v),
+              self._s(stream), C.byref(out))
+        return out.value
+
+    def release_prefix(self, node: int):
+        _call("halo_prefix_release", self.handle, node)
+
+    def read_prefix(self, node: int, k_out, v_out, stream=None):
+        _call("halo_prefix_read", self.handle, node, _ptr(k_out), _ptr(v_out), self._s(stream))
+
+    def node_info(self, node: int) -> dict:
+        parent, ntok, nb = C.c_int64(), C.c_int32(), C.c_int32()
+        _call("halo_node_info", self.handle, node, C.byref(parent), C.byref(ntok), C.byref(nb), None)
+        blocks = (C.c_int32 * max(nb.value, 1))()
+        _call("halo_node_info", self.handle, node, None, None, None, blocks)
+        return {"parent": parent.value, "ntok": ntok.value,
+                "blocks": list(blocks)[:nb.value]}
+
+    def open_request(self, leaf: int = -1) -> int:
+        out = C.c_int64()
+        _call("halo_request_open", self.handle, leaf, C.byref(out))
+        return out.value
+
+    def close_request(self, req: int):
+        _call("halo_request_close", self.handle, req)
+
+    def request_info(self, req: int) -> dict:
+        leaf, ln, nb = C.c_int64(), C.c_int32(), C.c_int32()
+        _call("halo_request_info", self.handle, req, C.byref(leaf), C.byref(ln), C.byref(nb))
+        return {"leaf": leaf.value, "suffix_len": ln.value, "nblocks": nb.value}
+
+    def append(self, reqs, ntok, k=None, v=None, stream=None):
+        _call("halo_suffix_append", self.handle, len(reqs), _i64_array(reqs), _i32_array(ntok),
+              _ptr(k), _ptr(v), self._s(stream))
+
+    def truncate(self, reqs, ntok):
+        _call("halo_suffix_truncate", self.handle, len(reqs), _i64_array(reqs), _i32_array(ntok))
+
+    def plan(self, reqs, options: PlanOptions | None = None, stream=None, reuse: "Plan" = None):
+        h = C.c_void_p(reuse.handle.value if reuse is not None else None)
+        _call("halo_decode_plan", self.handle, len(reqs), _i64_array(reqs),
+              C.byref(options) if options is not None else None, self._s(stream), C.byref(h))
+        if reuse is not None:
+            reuse.nreq = len(reqs)
+            return reuse
+        return Plan(self, h, len(reqs))
+
+    # ---- migration ----
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(uid, 128)
+        _call("halo_comm_init", self.handle, buf, nranks, rank)
+
+    def migrate_send(self, node: int, dst_rank: int, mode: int = 1, stream=None):
+        _call("halo_migrate_send", self.handle, node, dst_rank, mode, self._s(stream))
+
+    def migrate_recv(self, src_rank: int, parent: int, ntok: int, stream=None) -> int:
+        out = C.c_int64()
+        _call("halo_migrate_recv", self.handle, src_rank, parent, ntok, self._s(stream),
+              C.byref(out))
+        return out.value
+
+    def clone_prefix(self, node: int, dst: "Pool", parent: int = -1, stream=None) -> int:
+        out = C.c_int64()
+        _call("halo_prefix_clone", self.handle, node, dst.handle, parent, self._s(stream),
+              C.byref(out))
+        return out.value
+
+
+EXPORTS = {"req_order": 0, "tiles": 1, "req_nslots": 2, "unit_req": 3, "req_blk_off": 4,
+           "req_blk": 5}
+
+
+class Plan:
+    """One decode step's plan (halo_decode_plan); run it per layer (halo_decode_run)."""
+
+    def __init__(self, pool: Pool, handle, nreq: int):
+        self.pool, self.handle, self.nreq = pool, handle, nreq
+
+    def run(self, layer: int, q, out, lse=None, scale: float = 0.0, stream=None):
+        _call("halo_decode_run", self.handle, layer, _ptr(q), _ptr(out), _ptr(lse), scale,
+              self.pool._s(stream))
+
+    def run_stages(self, layer: int, mask: int, q, out=None, lse=None, scale: float = 0.0,
+                   stream=None):
+        _call("halo_decode_run_stages", self.handle, layer, mask, _ptr(q), _ptr(out), _ptr(lse),
+              scale, self.pool._s(stream))
+
+    def run_layers(self, nlayers: int, q, out, lse=None, scale: float = 0.0, stream=None):
+        _call("halo_decode_layers", self.handle, nlayers, _ptr(q), _ptr(out), _ptr(lse), scale,
+              self.pool._s(stream))
+
+    def info(self) -> dict:
+        inf = PlanInfo()
+        _call("halo_plan_get_info", self.handle, C.byref(inf))
+        return {name: getattr(inf, name) for name, _ in PlanInfo._fields_}
+
+    def export(self, which: str) -> np.ndarray:
+        code = EXPORTS[which]
+        n = C.c_int64()
+        _call("halo_plan_export", self.handle, code, None, 0, C.byref(n))
+        dt = np.uint32 if which == "req_blk" else np.int32
+        arr = np.zeros(max(n.value, 1), dtype=dt)
+        _call("halo_plan_export", self.handle, code, arr.ctypes.data, n.value, C.byref(n))
+        arr = arr[:n.value]
+        return arr.reshape(-1, 8) if which == "tiles" else arr
+
+    def destroy(self):
+        if self.handle:
+            _call("halo_plan_destroy", self.handle)
+            self.handle = None

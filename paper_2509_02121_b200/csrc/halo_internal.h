@@ -1,0 +1,69 @@
+// Internal declarations shared by the host runtime and the kernels of libhalo_attn.
+// (Product code only; the oracle shares nothing with this file.)
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace halo {
+
+constexpr int kBlockTok = 16;       // tokens per KV block
+constexpr int kK1Rows = 128;        // K1 tile rows (UMMA M)
+constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
+constexpr int kBlkCountShift = 27;  // K2 block entry: block | (ntok-1) << 27
+constexpr uint32_t kBlkMask = (1u << kBlkCountShift) - 1;
+
+// One K1 work tile: rows [row0, row0+nrows) of node n's (request x q-head-in-group) row
+// space for kv head `kv_head`, tokens [tok_begin, tok_end) of the node.
+struct PrefixTile {
+    int32_t req_off;    // index into req_order of the tile's first request
+    int32_t nrows;      // valid rows (<= 128)
+    int32_t kv_head;
+    int32_t tok_begin;  // multiple of 128
+    int32_t tok_end;
+    int32_t blk_off;    // index into node_blocks of the node's block 0
+    int32_t slot;       // partial slot written by this tile
+    int32_t node;       // plan-local node index (diagnostics)
+};
+static_assert(sizeof(PrefixTile) == 32, "PrefixTile is exported as int32 x 8");
+
+// Device view of a plan (all pointers into one device buffer).
+struct PlanDev {
+    const PrefixTile *tiles;
+    const int32_t *req_order;    // caller indices, DFS order
+    const int32_t *node_blocks;  // block ids of K1 nodes
+    const int32_t *unit_req;     // K2 request order (caller indices, LPT)
+    const int32_t *req_blk_off;  // [nreq+1] CSR into req_blk, by caller index
+    const uint32_t *req_blk;     // block | (ntok-1) << 27
+    const int32_t *req_nslots;   // [nreq]
+    float *part_o;               // [max_slots][nreq][Hq][D]
+    float *part_lse;             // [max_slots][nreq][Hq]
+    int32_t ntiles, nreq, nunits, max_slots;
+};
+
+struct PoolGeom {
+    int32_t layers, hkv, hq, d;
+    int64_t cap;  // blocks per layer
+};
+
+// ---- launchers (kernels_*.cu) ----
+// K1: tcgen05/TMEM prefix attention -> normalised fp32 partials + lse (natural log).
+cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v,
+                               const PlanDev &p, const PoolGeom &g, int layer,
+                               const void *q, float scale, cudaStream_t s);
+// K2+K3: paged-suffix decode with the fused log-sum-exp merge of the K1 partials.
+cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void *pool_k,
+                                 const void *pool_v, int layer, const void *q, float *out,
+                                 float *lse, float scale, int num_sms, cudaStream_t s);
+// K5 / K4-unpack: rows src[layer][i][head][:] -> pool slot slots[i] (i < n_copy); slots
+// [n_copy, n_copy+n_zero) are zero-filled.  src has `src_rows` rows per layer.
+cudaError_t launch_kv_scatter(const PoolGeom &g, void *pool_k, void *pool_v, const void *src_k,
+                              const void *src_v, int64_t src_rows, const int32_t *slots,
+                              int64_t n_copy, int64_t n_zero, int layer_begin, int layer_end,
+                              int num_sms, cudaStream_t s);
+// K4 pack: pool slot slots[i] -> dst[layer - layer_begin][i][head][:], i < n.
+cudaError_t launch_kv_gather(const PoolGeom &g, const void *pool_k, const void *pool_v,
+                             void *dst_k, void *dst_v, const int32_t *slots, int64_t n,
+                             int layer_begin, int layer_end, int num_sms, cudaStream_t s);
+
+}  // namespace halo

@@ -1,0 +1,170 @@
+// K4 (pack / unpack) and K5 (append) -- bitwise KV copies between the exchange layout
+// [layer][token][kv_head][d] (standardised KV state at operator boundaries)
+// and the paged pool [layer][block][kv_head][16][d] (block-level management).
+//
+// HBM-bound: every byte is read once and written once with 16-byte vector accesses.
+// Thread layout: one CTA row covers `tpb` tokens x (hkv heads x d/8 chunks); a thread's
+// (head, chunk, token lane) is fixed, so the only per-iteration index math is one slot
+// load and two multiply-adds.  Consecutive lanes touch consecutive 16-B chunks of a
+// token row, so both sides are coalesced (256-B runs per head at d=128).  Each thread
+// keeps kUnroll independent loads in flight; gridDim.x x layers is sized to a multiple
+// of the SM count.
+#include "halo_internal.h"
+
+namespace halo {
+namespace {
+
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ int4 ld_stream(const int4 *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+struct Geo {
+    int64_t n;          // tokens addressed
+    int32_t hkv, cpr;   // heads, 16-B chunks per head row (d/8)
+    int32_t tpb;        // tokens per CTA iteration
+    int64_t pool_layer; // int4 chunks per pool layer
+    int64_t src_rows;   // rows per layer in the exchange tensor
+};
+
+// Pool chunk of (layer, slot, head h, chunk e): ((layer*cap + blk)*hkv + h)*16 + off rows.
+__device__ __forceinline__ int64_t pool_chunk(const Geo &g, int layer, int32_t slot, int h,
+                                              int e) {
+    const int64_t blk = slot >> 4, off = slot & 15;
+    return (int64_t)layer * g.pool_layer + ((blk * g.hkv + h) * 16 + off) * g.cpr + e;
+}
+
+// src/dst exchange rows: [layer][i][h][chunk]
+__global__ void kv_scatter_kernel(int4 *__restrict__ pk, int4 *__restrict__ pv,
+                                  const int4 *__restrict__ sk, const int4 *__restrict__ sv,
+                                  Geo g, const int32_t *__restrict__ slots, int64_t n_copy,
+                                  int layer_begin) {
+    const int inner = g.hkv * g.cpr;
+    const int lane_tok = threadIdx.x / inner;
+    if (lane_tok >= g.tpb) return;
+    const int h = (threadIdx.x % inner) / g.cpr, e = threadIdx.x % g.cpr;
+    const int layer = layer_begin + blockIdx.y;
+    const int64_t step = (int64_t)gridDim.x * g.tpb;
+    const int64_t src_layer = (int64_t)blockIdx.y * g.src_rows;
+    for (int64_t i0 = (int64_t)blockIdx.x * g.tpb + lane_tok; i0 < g.n; i0 += step * kUnroll) {
+        int4 vk[kUnroll], vv[kUnroll];
+        int64_t dst[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t i = i0 + u * step;
+            dst[u] = -1;
+            if (i < g.n) {
+                dst[u] = pool_chunk(g, layer, slots[i], h, e);
+                if (i < n_copy) {
+                    const int64_t s = ((src_layer + i) * g.hkv + h) * g.cpr + e;
+                    vk[u] = ld_stream(sk + s);
+                    vv[u] = ld_stream(sv + s);
+                } else {
+                    vk[u] = make_int4(0, 0, 0, 0);
+                    vv[u] = vk[u];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (dst[u] >= 0) {
+                pk[dst[u]] = vk[u];
+                pv[dst[u]] = vv[u];
+            }
+        }
+    }
+}
+
+__global__ void kv_gather_kernel(const int4 *__restrict__ pk, const int4 *__restrict__ pv,
+                                 int4 *__restrict__ dk, int4 *__restrict__ dv, Geo g,
+                                 const int32_t *__restrict__ slots, int layer_begin) {
+    const int inner = g.hkv * g.cpr;
+    const int lane_tok = threadIdx.x / inner;
+    if (lane_tok >= g.tpb) return;
+    const int h = (threadIdx.x % inner) / g.cpr, e = threadIdx.x % g.cpr;
+    const int layer = layer_begin + blockIdx.y;
+    const int64_t step = (int64_t)gridDim.x * g.tpb;
+    const int64_t dst_layer = (int64_t)blockIdx.y * g.n;
+    for (int64_t i0 = (int64_t)blockIdx.x * g.tpb + lane_tok; i0 < g.n; i0 += step * kUnroll) {
+        int4 vk[kUnroll], vv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t i = i0 + u * step;
+            if (i < g.n) {
+                const int64_t s = pool_chunk(g, layer, slots[i], h, e);
+                vk[u] = ld_stream(pk + s);
+                vv[u] = ld_stream(pv + s);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t i = i0 + u * step;
+            if (i < g.n) {
+                const int64_t d = ((dst_layer + i) * g.hkv + h) * g.cpr + e;
+                dk[d] = vk[u];
+                dv[d] = vv[u];
+            }
+        }
+    }
+}
+
+// Block shape: `inner` = hkv*cpr threads per token; up to 256 threads (or one token row
+// if wider).  Grid: enough CTAs per layer that layers x gx ~ 8 CTAs per SM.
+void shape(const PoolGeom &pg, int64_t n, int layers, int num_sms, Geo &g, dim3 &grid,
+           int &threads) {
+    g.hkv = pg.hkv;
+    g.cpr = pg.d / 8;
+    const int inner = g.hkv * g.cpr;
+    g.tpb = inner >= 256 ? 1 : 256 / inner;
+    threads = g.tpb * inner;
+    g.n = n;
+    g.pool_layer = pg.cap * pg.hkv * 16 * g.cpr;
+    const int64_t per_layer_ctas = (n + (int64_t)g.tpb * kUnroll - 1) / ((int64_t)g.tpb * kUnroll);
+    int64_t want = ((int64_t)num_sms * 8 + layers - 1) / layers;
+    if (want > per_layer_ctas) want = per_layer_ctas;
+    if (want < 1) want = 1;
+    grid = dim3((unsigned)want, (unsigned)layers, 1);
+}
+
+}  // namespace
+
+cudaError_t launch_kv_scatter(const PoolGeom &pg, void *pool_k, void *pool_v, const void *src_k,
+                              const void *src_v, int64_t src_rows, const int32_t *slots,
+                              int64_t n_copy, int64_t n_zero, int layer_begin, int layer_end,
+                              int num_sms, cudaStream_t s) {
+    const int64_t n = n_copy + n_zero;
+    const int layers = layer_end - layer_begin;
+    if (n == 0 || layers <= 0) return cudaSuccess;
+    Geo g;
+    dim3 grid;
+    int threads;
+    shape(pg, n, layers, num_sms, g, grid, threads);
+    g.src_rows = src_rows;
+    kv_scatter_kernel<<<grid, threads, 0, s>>>((int4 *)pool_k, (int4 *)pool_v,
+                                               (const int4 *)src_k, (const int4 *)src_v, g,
+                                               slots, n_copy, layer_begin);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kv_gather(const PoolGeom &pg, const void *pool_k, const void *pool_v,
+                             void *dst_k, void *dst_v, const int32_t *slots, int64_t n,
+                             int layer_begin, int layer_end, int num_sms, cudaStream_t s) {
+    const int layers = layer_end - layer_begin;
+    if (n == 0 || layers <= 0) return cudaSuccess;
+    Geo g;
+    dim3 grid;
+    int threads;
+    shape(pg, n, layers, num_sms, g, grid, threads);
+    g.src_rows = n;
+    kv_gather_kernel<<<grid, threads, 0, s>>>((const int4 *)pool_k, (const int4 *)pool_v,
+                                              (int4 *)dst_k, (int4 *)dst_v, g, slots,
+                                              layer_begin);
+    return cudaGetLastError();
+}
+
+}  // namespace halo

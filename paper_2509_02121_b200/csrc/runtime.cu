@@ -1,0 +1,1367 @@
+// Host runtime + C ABI of libhalo_attn: paged KV pool, prefix-node registry, requests,
+// the decode-step planner, and NCCL migration.  See include/halo_attn.h for the contract
+// and DESIGN.md for the design.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "runtime.h"
+
+using namespace halo;
+
+namespace {
+
+thread_local std::string g_err;
+
+halo_status fail(halo_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define HALO_CUDA(expr)                                                                       \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(HALO_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));         \
+    } while (0)
+
+#define HALO_NCCL(expr)                                                                       \
+    do {                                                                                      \
+        if (!nccl().ok) return fail(HALO_ENCCL, "libnccl.so.2 not available");               \
+        ncclResult_t r_ = (expr);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(HALO_ENCCL, "%s failed: %s", #expr, nccl().GetErrorString(r_));      \
+    } while (0)
+
+#define HALO_GUARD_BEGIN try {
+#define HALO_GUARD_END                                                                        \
+    }                                                                                         \
+    catch (const std::bad_alloc &) {                                                          \
+        return fail(HALO_ENOMEM, "host allocation failed");                                  \
+    }                                                                                         \
+    catch (...) {                                                                             \
+        return fail(HALO_EINVAL, "internal error");                                          \
+    }
+
+struct DeviceGuard {
+    int prev = -1;
+    bool active = false;
+    explicit DeviceGuard(const halo_pool p) {
+        if (p && !p->host_only) {
+            cudaGetDevice(&prev);
+            if (prev != p->cfg.device) {
+                cudaSetDevice(p->cfg.device);
+                active = true;
+            }
+        }
+    }
+    ~DeviceGuard() {
+        if (active) cudaSetDevice(prev);
+    }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+size_t storage_bytes(const halo_pool_config &c) {
+    return (size_t)c.num_layers * (size_t)c.capacity_blocks * (size_t)c.num_kv_heads *
+           (size_t)kBlockTok * (size_t)c.head_dim * 2;
+}
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------- NCCL (resolved at run time)
+// The library does not link NCCL: it binds to the libnccl.so.2 already loaded in the
+// process (torch's), or loads one on first use.  This keeps the .so loadable everywhere
+// and avoids two NCCL versions in one process.
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi &nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+        a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+        a.Send = (decltype(a.Send))dlsym(h, "ncclSend");
+        a.Recv = (decltype(a.Recv))dlsym(h, "ncclRecv");
+        a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GetErrorString;
+        return a;
+    }();
+    return api;
+}
+
+// ---------------------------------------------------------------- block allocator
+cudaEvent_t get_event(halo_pool p) {
+    if (!p->event_cache.empty()) {
+        cudaEvent_t e = p->event_cache.back();
+        p->event_cache.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+}
+
+void note_stream(halo_pool p, cudaStream_t s) {
+    if (p->host_only) return;
+    ++p->use_clock;
+    for (auto &f : p->streams)
+        if (f.stream == s) {
+            f.last_use = p->use_clock;
+            return;
+        }
+    if (p->streams.size() >= 8) {
+        auto it = std::min_element(p->streams.begin(), p->streams.end(),
+                                   [](const StreamFence &a, const StreamFence &b) {
+                                       return a.last_use < b.last_use;
+                                   });
+        *it = StreamFence{s, p->use_clock};
+    } else {
+        p->streams.push_back(StreamFence{s, p->use_clock});
+    }
+}
+
+void reclaim(halo_pool p, bool wait) {
+    for (size_t i = 0; i < p->pending.size();) {
+        PendingFree &pf = p->pending[i];
+        bool done = true;
+        for (cudaEvent_t e : pf.events) {
+            cudaError_t r = wait ? cudaEventSynchronize(e) : cudaEventQuery(e);
+            if (r == cudaErrorNotReady) {
+                done = false;
+                break;
+            }
+            if (r != cudaSuccess) cudaGetLastError();
+        }
+        if (!done) {
+            ++i;
+            continue;
+        }
+        for (auto it = pf.blocks.rbegin(); it != pf.blocks.rend(); ++it) p->free_list.push_back(*it);
+        for (cudaEvent_t e : pf.events) p->event_cache.push_back(e);
+        p->pending.erase(p->pending.begin() + i);
+    }
+}
+
+halo_status alloc_blocks(halo_pool p, int64_t n, std::vector<int32_t> &out) {
+    if ((int64_t)p->free_list.size() < n) reclaim(p, false);
+    if ((int64_t)p->free_list.size() < n) reclaim(p, true);
+    if ((int64_t)p->free_list.size() < n)
+        return fail(HALO_ENOMEM, "pool out of blocks: need %lld, free %lld", (long long)n,
+                    (long long)p->free_list.size());
+    out.reserve(out.size() + n);
+    for (int64_t i = 0; i < n; ++i) {
+        out.push_back(p->free_list.back());
+        p->free_list.pop_back();
+    }
+    return HALO_OK;
+}
+
+// Return blocks that were never handed to the device (error paths).
+void unalloc_blocks(halo_pool p, const std::vector<int32_t> &blocks, size_t from) {
+    for (size_t i = blocks.size(); i > from; --i) p->free_list.push_back(blocks[i - 1]);
+}
+
+// Blocks become reusable once the work enqueued so far on every stream that used the
+// pool has passed (events recorded now).
+void release_blocks(halo_pool p, std::vector<int32_t> &&blocks) {
+    if (blocks.empty()) return;
+    if (p->host_only) {
+        for (auto it = blocks.rbegin(); it != blocks.rend(); ++it) p->free_list.push_back(*it);
+        return;
+    }
+    PendingFree pf;
+    pf.blocks = std::move(blocks);
+    for (auto &f : p->streams) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(f.stream, &cs) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (cs != cudaStreamCaptureStatusNone) continue;
+        cudaEvent_t e = get_event(p);
+        if (e && cudaEventRecord(e, f.stream) == cudaSuccess) pf.events.push_back(e);
+        else cudaGetLastError();
+    }
+    p->pending.push_back(std::move(pf));
+}
+
+// ---------------------------------------------------------------- device scratch
+struct Scratch {
+    void *ptr = nullptr;
+    cudaStream_t s = nullptr;
+    ~Scratch() {
+        if (ptr) cudaFreeAsync(ptr, s);
+    }
+};
+
+halo_status upload(const void *host, size_t bytes, cudaStream_t s, Scratch &sc) {
+    sc.s = s;
+    HALO_CUDA(cudaMallocAsync(&sc.ptr, bytes ? bytes : 16, s));
+    if (bytes) HALO_CUDA(cudaMemcpyAsync(sc.ptr, host, bytes, cudaMemcpyHostToDevice, s));
+    return HALO_OK;
+}
+
+// Device copy of a host-or-device input.
+halo_status as_device(const void *p, size_t bytes, cudaStream_t s, Scratch &sc, const void **out) {
+    if (is_device_ptr(p)) {
+        *out = p;
+        return HALO_OK;
+    }
+    halo_status st = upload(p, bytes, s, sc);
+    if (st != HALO_OK) return st;
+    *out = sc.ptr;
+    return HALO_OK;
+}
+
+halo_status check_pool(halo_pool p) {
+    if (!p) return fail(HALO_EINVAL, "null pool");
+    return HALO_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+halo_status make_tmap(halo_pool p, void *base, CUtensorMap *out) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        HALO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess)
+            return fail(HALO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)f;
+    }
+    const auto &c = p->cfg;
+    // dims (innermost first): d, token-in-block, kv head, layer*capacity + block
+    cuuint64_t dims[4] = {(cuuint64_t)c.head_dim, (cuuint64_t)kBlockTok, (cuuint64_t)c.num_kv_heads,
+                          (cuuint64_t)c.num_layers * (cuuint64_t)c.capacity_blocks};
+    cuuint64_t strides[3] = {(cuuint64_t)c.head_dim * 2, (cuuint64_t)kBlockTok * c.head_dim * 2,
+                             (cuuint64_t)c.num_kv_heads * kBlockTok * c.head_dim * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)kBlockTok, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HALO_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return HALO_OK;
+}
+
+// ---------------------------------------------------------------- plan builder
+struct PNode {
+    int64_t id;
+    int parent;  // plan-local index or -1
+    const Node *node;
+    std::vector<int> children;
+    int pre = 0, end = 0;  // preorder interval [pre, end)
+    int r0 = 0, r1 = 0;    // request range in DFS order
+    bool tensor = false;
+    int splits = 0, chunk = 0;
+    int slot_base = 0;
+    int blk_off = 0;
+};
+
+// Choose a split-N chunk (tokens, multiple of 128) for the K1 nodes so the tiles fill the
+// SMs: minimise an estimated makespan  max(longest tile, waves x mean tile)  where a tile
+// costs its tokens plus a fixed per-tile overhead.
+int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_splits) {
+    int64_t max_tok = 0;
+    for (auto &n : ns)
+        if (n.tensor) max_tok = std::max<int64_t>(max_tok, n.node->ntok);
+    if (max_tok == 0) return kK1Tok;
+    const int64_t kOvh = 256;
+    const int64_t nk = ceil_div(max_tok, kK1Tok);
+    const int64_t step = std::max<int64_t>(1, nk / 256);
+    double best = 1e300;
+    int best_c = (int)(nk * kK1Tok);
+    for (int64_t k = nk; k >= 1; k -= step) {
+        const int64_t C = k * kK1Tok;
+        int64_t T = 0;
+        double sum = 0, maxc = 0;
+        for (auto &n : ns) {
+            if (!n.tensor) continue;
+            const int64_t tok = n.node->ntok;
+            int64_t s = std::min<int64_t>(ceil_div(tok, C), max_splits);
+            const int64_t ch = ceil_div(ceil_div(tok, s), kK1Tok) * kK1Tok;
+            s = ceil_div(tok, ch);
+            const int64_t base = ceil_div((int64_t)(n.r1 - n.r0) * g, kK1Rows) * hkv;
+            const double cost = (double)std::min(ch, tok) + kOvh;
+            T += base * s;
+            sum += (double)(base * s) * cost;
+            maxc = std::max(maxc, cost);
+        }
+        const double est = std::max(maxc, (double)ceil_div(T, nsm) * (sum / (double)T));
+        if (est < best * 0.999) {
+            best = est;
+            best_c = (int)C;
+        }
+    }
+    return best_c;
+}
+
+halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
+    halo_pool p = pl->pool;
+    const auto &cfg = p->cfg;
+    const int g = cfg.num_q_heads / cfg.num_kv_heads;
+    const int hkv = cfg.num_kv_heads, hq = cfg.num_q_heads, D = cfg.head_dim;
+    const int min_rows = pl->opt.min_tensor_rows > 0 ? pl->opt.min_tensor_rows : 64;
+    const int max_splits = pl->opt.max_splits > 0 ? pl->opt.max_splits : 16;
+
+    // 1. requests
+    std::vector<const Request *> R(nreq);
+    for (int i = 0; i < nreq; ++i) {
+        auto it = p->requests.find(reqs[i]);
+        if (it == p->requests.end())
+            return fail(HALO_ENOENT, "unknown request id %lld", (long long)reqs[i]);
+        if (it->second.leaf < 0 && it->second.len == 0)
+            return fail(HALO_EINVAL, "request %lld has an empty context", (long long)reqs[i]);
+        R[i] = &it->second;
+    }
+    // 2. involved nodes
+    std::vector<PNode> ns;
+    std::unordered_map<int64_t, int> loc;
+    std::vector<int> leaf_loc(nreq, -1);
+    for (int i = 0; i < nreq; ++i) {
+        int64_t id = R[i]->leaf;
+        int child = -1;
+        while (id >= 0) {
+            auto f = loc.find(id);
+            if (f != loc.end()) {
+                if (child >= 0) ns[child].parent = f->second;
+                if (leaf_loc[i] < 0) leaf_loc[i] = f->second;
+                break;
+            }
+            auto nit = p->nodes.find(id);
+            if (nit == p->nodes.end()) return fail(HALO_EINVAL, "dangling node %lld", (long long)id);
+            PNode pn;
+            pn.id = id;
+            pn.parent = -1;
+            pn.node = &nit->second;
+            ns.push_back(pn);
+            const int me = (int)ns.size() - 1;
+            loc[id] = me;
+            if (child >= 0) ns[child].parent = me;
+            if (leaf_loc[i] < 0) leaf_loc[i] = me;
+            child = me;
+            id = nit->second.parent;
+        }
+    }
+    // deterministic child order: by node id
+    std::vector<int> roots;
+    {
+        std::vector<int> by_id(ns.size());
+        for (size_t i = 0; i < ns.size(); ++i) by_id[i] = (int)i;
+        std::sort(by_id.begin(), by_id.end(), [&](int a, int b) { return ns[a].id < ns[b].id; });
+        for (int i : by_id) {
+            if (ns[i].parent < 0) roots.push_back(i);
+            else ns[ns[i].parent].children.push_back(i);
+        }
+    }
+    // 3. DFS preorder
+    std::vector<int> pre_order;
+    {
+        std::vector<std::pair<int, int>> st;  // (node, next child)
+        for (int r : roots) {
+            st.push_back({r, 0});
+            ns[r].pre = (int)pre_order.size();
+            pre_order.push_back(r);
+            while (!st.empty()) {
+                auto &top = st.back();
+                PNode &n = ns[top.first];
+                if (top.second < (int)n.children.size()) {
+                    const int c = n.children[top.second++];
+                    ns[c].pre = (int)pre_order.size();
+                    pre_order.push_back(c);
+                    st.push_back({c, 0});
+                } else {
+                    n.end = (int)pre_order.size();
+                    st.pop_back();
+                }
+            }
+        }
+    }
+    // 4. requests in DFS order of their leaves (no-prefix requests last)
+    std::vector<int> key(nreq);
+    for (int i = 0; i < nreq; ++i) key[i] = leaf_loc[i] >= 0 ? ns[leaf_loc[i]].pre : INT32_MAX;
+    pl->req_order.resize(nreq);
+    for (int i = 0; i < nreq; ++i) pl->req_order[i] = i;
+    std::stable_sort(pl->req_order.begin(), pl->req_order.end(),
+                     [&](int a, int b) { return key[a] < key[b]; });
+    std::vector<int> sorted_keys(nreq);
+    for (int i = 0; i < nreq; ++i) sorted_keys[i] = key[pl->req_order[i]];
+    // 5./6. node request ranges and the K1 decision
+    int tensor_nodes = 0;
+    for (auto &n : ns) {
+        n.r0 = (int)(std::lower_bound(sorted_keys.begin(), sorted_keys.end(), n.pre) - sorted_keys.begin());
+        n.r1 = (int)(std::lower_bound(sorted_keys.begin(), sorted_keys.end(), n.end) - sorted_keys.begin());
+        n.tensor = (int64_t)(n.r1 - n.r0) * g >= min_rows;
+        tensor_nodes += n.tensor;
+    }
+    // 7. splits
+    if (pl->opt.force_splits > 0) {
+        for (auto &n : ns) {
+            if (!n.tensor) continue;
+            const int64_t tok = n.node->ntok;
+            const int64_t s = std::min<int64_t>(pl->opt.force_splits, ceil_div(tok, kK1Tok));
+            n.chunk = (int)(ceil_div(ceil_div(tok, s), kK1Tok) * kK1Tok);
+            n.splits = (int)ceil_div(tok, n.chunk);
+        }
+    } else {
+        const int C = choose_chunk(ns, g, hkv, p->num_sms, max_splits);
+        for (auto &n : ns) {
+            if (!n.tensor) continue;
+            const int64_t tok = n.node->ntok;
+            const int64_t s = std::min<int64_t>(ceil_div(tok, C), max_splits);
+            n.chunk = (int)(ceil_div(ceil_div(tok, s), kK1Tok) * kK1Tok);
+            n.splits = (int)ceil_div(tok, n.chunk);
+        }
+    }
+    // 8. slot bases along each path (preorder visits parents first)
+    for (int i : pre_order) {
+        PNode &n = ns[i];
+        n.slot_base = n.parent < 0 ? 0
+                                   : ns[n.parent].slot_base + (ns[n.parent].tensor ? ns[n.parent].splits : 0);
+    }
+    pl->req_nslots.assign(nreq, 0);
+    int max_slots = 0;
+    for (int i = 0; i < nreq; ++i) {
+        if (leaf_loc[i] >= 0) {
+            const PNode &lf = ns[leaf_loc[i]];
+            pl->req_nslots[i] = lf.slot_base + (lf.tensor ? lf.splits : 0);
+        }
+        max_slots = std::max(max_slots, pl->req_nslots[i]);
+    }
+    // 9./10. K1 node blocks and tiles
+    pl->node_blocks.clear();
+    pl->tiles.clear();
+    double k1_flops = 0, k1_bytes = 0;
+    for (int i : pre_order) {
+        PNode &n = ns[i];
+        if (!n.tensor) continue;
+        n.blk_off = (int)pl->node_blocks.size();
+        pl->node_blocks.insert(pl->node_blocks.end(), n.node->blocks.begin(), n.node->blocks.end());
+        const int64_t rows = (int64_t)(n.r1 - n.r0) * g;
+        const int64_t tok = n.node->ntok;
+        k1_flops += 4.0 * rows * tok * D * hkv;
+        k1_bytes += (double)tok * hkv * D * 2 * 2 + (double)rows * hkv * D * 2 +
+                    (double)rows * hkv * (D + 1) * 4 * n.splits;
+        for (int64_t m0 = 0; m0 < rows; m0 += kK1Rows)
+            for (int j = 0; j < hkv; ++j)
+                for (int s = 0; s < n.splits; ++s) {
+                    PrefixTile t;
+                    t.req_off = n.r0 + (int32_t)(m0 / g);
+                    t.nrows = (int32_t)std::min<int64_t>(kK1Rows, rows - m0);
+                    t.kv_head = j;
+                    t.tok_begin = s * n.chunk;
+                    t.tok_end = (int32_t)std::min<int64_t>(tok, (int64_t)(s + 1) * n.chunk);
+                    t.blk_off = n.blk_off;
+                    t.slot = n.slot_base + s;
+                    t.node = i;
+                    pl->tiles.push_back(t);
+                }
+    }
+    std::stable_sort(pl->tiles.begin(), pl->tiles.end(), [](const PrefixTile &a, const PrefixTile &b) {
+        return (a.tok_end - a.tok_begin) > (b.tok_end - b.tok_begin);
+    });
+    // 11. K2 per-request block lists: folded path nodes root -> leaf, then the suffix
+    pl->req_blk_off.assign(nreq + 1, 0);
+    pl->req_blk.clear();
+    double k2_bytes = 0, unshared = 0;
+    std::vector<int> path;
+    auto push_blocks = [&](const std::vector<int32_t> &blocks, int32_t ntok) {
+        for (size_t b = 0; b < blocks.size(); ++b) {
+            const int32_t cnt = std::min<int32_t>(kBlockTok, ntok - (int32_t)b * kBlockTok);
+            pl->req_blk.push_back((uint32_t)blocks[b] | ((uint32_t)(cnt - 1) << kBlkCountShift));
+        }
+    };
+    int folded = 0;
+    for (auto &n : ns) folded += !n.tensor;
+    for (int i = 0; i < nreq; ++i) {
+        pl->req_blk_off[i] = (int32_t)pl->req_blk.size();
+        path.clear();
+        for (int x = leaf_loc[i]; x >= 0; x = ns[x].parent) path.push_back(x);
+        int64_t ctx = R[i]->len;
+        for (auto it = path.rbegin(); it != path.rend(); ++it) {
+            const PNode &n = ns[*it];
+            ctx += n.node->ntok;
+            if (!n.tensor) push_blocks(n.node->blocks, n.node->ntok);
+        }
+        push_blocks(R[i]->blocks, R[i]->len);
+        unshared += (double)ctx * hkv * D * 4;
+    }
+    pl->req_blk_off[nreq] = (int32_t)pl->req_blk.size();
+    k2_bytes = (double)pl->req_blk.size() * kBlockTok * hkv * D * 4 + (double)nreq * hq * D * 2 +
+               (double)nreq * hq * (D + 1) * 4;
+    for (int i = 0; i < nreq; ++i) k2_bytes += (double)pl->req_nslots[i] * hq * (D + 1) * 4;
+    // 12. K2 request order: longest block list first (LPT), stable
+    pl->unit_req.resize(nreq);
+    for (int i = 0; i < nreq; ++i) pl->unit_req[i] = i;
+    std::stable_sort(pl->unit_req.begin(), pl->unit_req.end(), [&](int a, int b) {
+        return pl->req_blk_off[a + 1] - pl->req_blk_off[a] > pl->req_blk_off[b + 1] - pl->req_blk_off[b];
+    });
+    // 13. info
+    halo_plan_info &inf = pl->info;
+    inf = halo_plan_info{};
+    inf.nreq = nreq;
+    inf.num_q_heads = hq;
+    inf.num_kv_heads = hkv;
+    inf.head_dim = D;
+    inf.tensor_nodes = tensor_nodes;
+    inf.folded_nodes = folded;
+    inf.k1_tiles = (int32_t)pl->tiles.size();
+    inf.k2_units = nreq * hkv;
+    inf.max_slots = max_slots;
+    inf.k1_flops = k1_flops;
+    inf.k1_bytes = k1_bytes;
+    inf.k2_bytes = k2_bytes;
+    inf.unshared_bytes = unshared;
+    pl->nreq = nreq;
+    return HALO_OK;
+}
+
+size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+halo_status upload_plan(halo_plan pl, cudaStream_t s) {
+    halo_pool p = pl->pool;
+    const int nreq = pl->nreq;
+    size_t off = 0;
+    const size_t o_tiles = off; off = align16(off + pl->tiles.size() * sizeof(PrefixTile));
+    const size_t o_order = off; off = align16(off + nreq * 4);
+    const size_t o_nblk = off; off = align16(off + pl->node_blocks.size() * 4);
+    const size_t o_unit = off; off = align16(off + nreq * 4);
+    const size_t o_boff = off; off = align16(off + (nreq + 1) * 4);
+    const size_t o_blk = off; off = align16(off + pl->req_blk.size() * 4);
+    const size_t o_nsl = off; off = align16(off + nreq * 4);
+    const size_t total = off;
+    pl->host_buf.resize(total);
+    uint8_t *h = pl->host_buf.data();
+    auto put = [&](size_t o, const void *src, size_t n) { if (n) memcpy(h + o, src, n); };
+    put(o_tiles, pl->tiles.data(), pl->tiles.size() * sizeof(PrefixTile));
+    put(o_order, pl->req_order.data(), nreq * 4);
+    put(o_nblk, pl->node_blocks.data(), pl->node_blocks.size() * 4);
+    put(o_unit, pl->unit_req.data(), nreq * 4);
+    put(o_boff, pl->req_blk_off.data(), (nreq + 1) * 4);
+    put(o_blk, pl->req_blk.data(), pl->req_blk.size() * 4);
+    put(o_nsl, pl->req_nslots.data(), nreq * 4);
+    if (p->host_only) return HALO_OK;
+
+    if (pl->dbuf_cap < total) {
+        if (pl->dbuf) {
+            HALO_CUDA(cudaStreamSynchronize(s));
+            cudaFree(pl->dbuf);
+            pl->dbuf = nullptr;
+        }
+        const size_t cap = total + total / 2 + 4096;
+        HALO_CUDA(cudaMalloc(&pl->dbuf, cap));
+        pl->dbuf_cap = cap;
+    }
+    const size_t part_elems = (size_t)pl->info.max_slots * nreq * p->cfg.num_q_heads * (p->cfg.head_dim + 1);
+    if (pl->part_cap < part_elems) {
+        if (pl->part) {
+            HALO_CUDA(cudaStreamSynchronize(s));
+            cudaFree(pl->part);
+            pl->part = nullptr;
+        }
+        const size_t cap = part_elems + part_elems / 4 + 1024;
+        HALO_CUDA(cudaMalloc(&pl->part, cap * 4));
+        pl->part_cap = cap;
+    }
+    HALO_CUDA(cudaMemcpyAsync(pl->dbuf, h, total, cudaMemcpyHostToDevice, s));
+    uint8_t *d = static_cast<uint8_t *>(pl->dbuf);
+    PlanDev &dv = pl->dev;
+    dv.tiles = reinterpret_cast<const PrefixTile *>(d + o_tiles);
+    dv.req_order = reinterpret_cast<const int32_t *>(d + o_order);
+    dv.node_blocks = reinterpret_cast<const int32_t *>(d + o_nblk);
+    dv.unit_req = reinterpret_cast<const int32_t *>(d + o_unit);
+    dv.req_blk_off = reinterpret_cast<const int32_t *>(d + o_boff);
+    dv.req_blk = reinterpret_cast<const uint32_t *>(d + o_blk);
+    dv.req_nslots = reinterpret_cast<const int32_t *>(d + o_nsl);
+    dv.part_o = pl->part;
+    dv.part_lse = pl->part + (size_t)pl->info.max_slots * nreq * p->cfg.num_q_heads * p->cfg.head_dim;
+    dv.ntiles = (int32_t)pl->tiles.size();
+    dv.nreq = nreq;
+    dv.nunits = nreq * p->cfg.num_kv_heads;
+    dv.max_slots = pl->info.max_slots;
+    return HALO_OK;
+}
+
+halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, float *lse,
+                      float scale, cudaStream_t s, int mask = 3) {
+    halo_pool p = pl->pool;
+    cudaError_t e;
+    if (mask & 1) {
+        e = launch_prefix_attn(&p->tmap_k, &p->tmap_v, pl->dev, p->geom, layer, q, scale, s);
+        if (e != cudaSuccess) return fail(HALO_ECUDA, "prefix kernel launch: %s", cudaGetErrorString(e));
+    }
+    if (mask & 2) {
+        e = launch_suffix_decode(pl->dev, p->geom, p->k, p->v, layer, q, out, lse, scale, p->num_sms, s);
+        if (e != cudaSuccess) return fail(HALO_ECUDA, "suffix kernel launch: %s", cudaGetErrorString(e));
+    }
+    return HALO_OK;
+}
+
+// Chunk of layers per migration message: ~32 MiB of K+V.
+int layers_per_chunk(halo_pool p, int32_t ntok) {
+    const size_t per_layer = (size_t)ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2 * 2;
+    size_t l = ((size_t)32 << 20) / std::max<size_t>(per_layer, 1);
+    if (l < 1) l = 1;
+    if (l > (size_t)p->cfg.num_layers) l = p->cfg.num_layers;
+    return (int)l;
+}
+
+halo_status ensure_mig(halo_pool p, size_t bytes) {
+    if (p->mig_cap >= bytes) return HALO_OK;
+    if (p->mig_buf) {
+        HALO_CUDA(cudaDeviceSynchronize());
+        cudaFree(p->mig_buf);
+        p->mig_buf = nullptr;
+    }
+    HALO_CUDA(cudaMalloc(&p->mig_buf, bytes));
+    p->mig_cap = bytes;
+    return HALO_OK;
+}
+
+std::vector<int32_t> token_slots(const std::vector<int32_t> &blocks, int64_t n) {
+    std::vector<int32_t> slots(n);
+    for (int64_t i = 0; i < n; ++i) slots[i] = blocks[i / kBlockTok] * kBlockTok + (int32_t)(i % kBlockTok);
+    return slots;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char *halo_last_error(void) { return g_err.c_str(); }
+int32_t halo_abi_version(void) { return HALO_ABI_VERSION; }
+
+size_t halo_pool_storage_bytes(const halo_pool_config *cfg) { return cfg ? storage_bytes(*cfg) : 0; }
+
+halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
+    HALO_GUARD_BEGIN
+    if (!cfg || !out) return fail(HALO_EINVAL, "null argument");
+    const auto &c = *cfg;
+    if (c.num_layers < 1 || c.num_kv_heads < 1 || c.num_kv_heads > 64 || c.num_q_heads < 1 ||
+        c.num_q_heads % c.num_kv_heads != 0)
+        return fail(HALO_EINVAL, "bad head/layer counts");
+    const int g = c.num_q_heads / c.num_kv_heads;
+    if (g != 1 && g != 2 && g != 4 && g != 8) return fail(HALO_EINVAL, "q heads per kv head must be 1, 2, 4 or 8");
+    if (c.head_dim != 64 && c.head_dim != 128) return fail(HALO_EINVAL, "head_dim must be 64 or 128");
+    if (c.block_tokens != kBlockTok) return fail(HALO_EINVAL, "block_tokens must be 16");
+    if (c.capacity_blocks < 1 || c.capacity_blocks > (int64_t)kBlkMask ||
+        (int64_t)c.num_layers * c.capacity_blocks >= ((int64_t)1 << 31))
+        return fail(HALO_EINVAL, "capacity_blocks out of range");
+    if ((c.k_storage == nullptr) != (c.v_storage == nullptr))
+        return fail(HALO_EINVAL, "k_storage and v_storage must both be set or both NULL");
+    auto *p = new halo_pool_s();
+    p->cfg = c;
+    p->host_only = c.device < 0;
+    p->geom = PoolGeom{c.num_layers, c.num_kv_heads, c.num_q_heads, c.head_dim, c.capacity_blocks};
+    p->free_list.reserve(c.capacity_blocks);
+    for (int64_t b = c.capacity_blocks - 1; b >= 0; --b) p->free_list.push_back((int32_t)b);
+    if (!p->host_only) {
+        DeviceGuard dg(p);
+        int dev_count = 0;
+        if (cudaGetDeviceCount(&dev_count) != cudaSuccess || c.device >= dev_count) {
+            cudaGetLastError();
+            delete p;
+            return fail(HALO_EINVAL, "no CUDA device %d", c.device);
+        }
+        cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+        const size_t bytes = storage_bytes(c);
+        if (c.k_storage) {
+            p->k = c.k_storage;
+            p->v = c.v_storage;
+        } else {
+            if (cudaMalloc(&p->k, bytes) != cudaSuccess || cudaMalloc(&p->v, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                if (p->k) cudaFree(p->k);
+                delete p;
+                return fail(HALO_ENOMEM, "cudaMalloc of %zu bytes x 2 failed", bytes);
+            }
+            p->own_storage = true;
+        }
+        halo_status st = HALO_OK;
+        if (cudaMemset(p->k, 0, bytes) != cudaSuccess || cudaMemset(p->v, 0, bytes) != cudaSuccess)
+            st = fail(HALO_ECUDA, "cudaMemset of the pool failed");
+        if (st == HALO_OK) st = make_tmap(p, p->k, &p->tmap_k);
+        if (st == HALO_OK) st = make_tmap(p, p->v, &p->tmap_v);
+        if (st != HALO_OK) {
+            if (p->own_storage) {
+                cudaFree(p->k);
+                cudaFree(p->v);
+            }
+            delete p;
+            return st;
+        }
+    }
+    *out = p;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_pool_destroy(halo_pool p) {
+    HALO_GUARD_BEGIN
+    if (!p) return fail(HALO_EINVAL, "null pool");
+    if (p->plans_alive > 0) return fail(HALO_EBUSY, "%d plan(s) still alive", p->plans_alive);
+    if (!p->host_only) {
+        DeviceGuard dg(p);
+        cudaDeviceSynchronize();
+        for (auto &pf : p->pending)
+            for (cudaEvent_t e : pf.events) cudaEventDestroy(e);
+        for (cudaEvent_t e : p->event_cache) cudaEventDestroy(e);
+        for (cudaEvent_t e : p->mig_ev)
+            if (e) cudaEventDestroy(e);
+        if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
+        if (p->side) cudaStreamDestroy(p->side);
+        if (p->mig_buf) cudaFree(p->mig_buf);
+        if (p->own_storage) {
+            cudaFree(p->k);
+            cudaFree(p->v);
+        }
+    }
+    delete p;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_pool_stats(halo_pool p, int64_t *free_blocks, int64_t *used_blocks) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    { DeviceGuard dg(p); reclaim(p, false); }
+    int64_t pend = 0;
+    for (auto &pf : p->pending) pend += (int64_t)pf.blocks.size();
+    if (free_blocks) *free_blocks = (int64_t)p->free_list.size();
+    if (used_blocks) *used_blocks = p->cfg.capacity_blocks - (int64_t)p->free_list.size() - pend;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_pool_storage(halo_pool p, void **k, void **v) {
+    if (check_pool(p)) return HALO_EINVAL;
+    if (k) *k = p->k;
+    if (v) *v = p->v;
+    return HALO_OK;
+}
+
+halo_status halo_prefix_register(halo_pool p, int64_t parent, int32_t ntok, const void *k,
+                                 const void *v, void *stream, int64_t *node_out) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!node_out || ntok < 1) return fail(HALO_EINVAL, "ntok must be >= 1 and node_out non-null");
+    if (parent >= 0 && !p->nodes.count(parent)) return fail(HALO_ENOENT, "unknown parent %lld", (long long)parent);
+    if (parent < -1) return fail(HALO_EINVAL, "bad parent id");
+    if (!p->host_only && (!k || !v)) return fail(HALO_EINVAL, "null k/v");
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nblk = ceil_div(ntok, kBlockTok);
+    std::vector<int32_t> blocks;
+    halo_status st = alloc_blocks(p, nblk, blocks);
+    if (st != HALO_OK) return st;
+    if (!p->host_only) {
+        const size_t bytes = (size_t)p->cfg.num_layers * ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
+        std::vector<int32_t> slots = token_slots(blocks, nblk * kBlockTok);
+        Scratch ss, sk, sv;
+        const void *dk = nullptr, *dvp = nullptr;
+        st = upload(slots.data(), slots.size() * 4, s, ss);
+        if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
+        if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
+        if (st == HALO_OK) {
+            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, ntok, (const int32_t *)ss.ptr, ntok,
+                                              nblk * kBlockTok - ntok, 0, p->cfg.num_layers, p->num_sms, s);
+            if (e != cudaSuccess) st = fail(HALO_ECUDA, "scatter launch: %s", cudaGetErrorString(e));
+        }
+        if (st != HALO_OK) {
+            unalloc_blocks(p, blocks, 0);
+            return st;
+        }
+        note_stream(p, s);
+    }
+    const int64_t id = p->next_id++;
+    Node n;
+    n.parent = parent;
+    n.ntok = ntok;
+    n.blocks = std::move(blocks);
+    p->nodes.emplace(id, std::move(n));
+    if (parent >= 0) p->nodes[parent].children++;
+    *node_out = id;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_prefix_release(halo_pool p, int64_t node) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (it->second.children || it->second.requests)
+        return fail(HALO_EBUSY, "node %lld has %d children and %d requests", (long long)node,
+                    it->second.children, it->second.requests);
+    DeviceGuard dg(p);
+    const int64_t parent = it->second.parent;
+    release_blocks(p, std::move(it->second.blocks));
+    p->nodes.erase(it);
+    if (parent >= 0) p->nodes[parent].children--;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_prefix_read(halo_pool p, int64_t node, void *k_out, void *v_out, void *stream) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (p->host_only) return fail(HALO_EUNSUPPORTED, "host-only pool");
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (!k_out || !v_out) return fail(HALO_EINVAL, "null output");
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<int32_t> slots = token_slots(it->second.blocks, it->second.ntok);
+    Scratch ss;
+    halo_status st = upload(slots.data(), slots.size() * 4, s, ss);
+    if (st != HALO_OK) return st;
+    cudaError_t e = launch_kv_gather(p->geom, p->k, p->v, k_out, v_out, (const int32_t *)ss.ptr,
+                                     it->second.ntok, 0, p->cfg.num_layers, p->num_sms, s);
+    if (e != cudaSuccess) return fail(HALO_ECUDA, "gather launch: %s", cudaGetErrorString(e));
+    note_stream(p, s);
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_node_info(halo_pool p, int64_t node, int64_t *parent, int32_t *ntok, int32_t *nblocks,
+                           int32_t *blocks_out) {
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (parent) *parent = it->second.parent;
+    if (ntok) *ntok = it->second.ntok;
+    if (nblocks) *nblocks = (int32_t)it->second.blocks.size();
+    if (blocks_out) memcpy(blocks_out, it->second.blocks.data(), it->second.blocks.size() * 4);
+    return HALO_OK;
+}
+
+halo_status halo_request_open(halo_pool p, int64_t leaf, int64_t *req_out) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!req_out) return fail(HALO_EINVAL, "null req_out");
+    if (leaf < -1) return fail(HALO_EINVAL, "bad leaf id");
+    if (leaf >= 0 && !p->nodes.count(leaf)) return fail(HALO_ENOENT, "unknown node %lld", (long long)leaf);
+    const int64_t id = p->next_id++;
+    Request r;
+    r.leaf = leaf;
+    p->requests.emplace(id, std::move(r));
+    if (leaf >= 0) p->nodes[leaf].requests++;
+    *req_out = id;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_request_close(halo_pool p, int64_t req) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->requests.find(req);
+    if (it == p->requests.end()) return fail(HALO_ENOENT, "unknown request %lld", (long long)req);
+    DeviceGuard dg(p);
+    const int64_t leaf = it->second.leaf;
+    release_blocks(p, std::move(it->second.blocks));
+    p->requests.erase(it);
+    if (leaf >= 0) p->nodes[leaf].requests--;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_request_info(halo_pool p, int64_t req, int64_t *leaf, int32_t *suffix_len, int32_t *nblocks) {
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->requests.find(req);
+    if (it == p->requests.end()) return fail(HALO_ENOENT, "unknown request %lld", (long long)req);
+    if (leaf) *leaf = it->second.leaf;
+    if (suffix_len) *suffix_len = it->second.len;
+    if (nblocks) *nblocks = (int32_t)it->second.blocks.size();
+    return HALO_OK;
+}
+
+halo_status halo_suffix_append(halo_pool p, int32_t nreq, const int64_t *reqs, const int32_t *ntok,
+                               const void *k, const void *v, void *stream) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (nreq < 0 || (nreq > 0 && (!reqs || !ntok))) return fail(HALO_EINVAL, "bad request list");
+    // simulate (handles repeated ids), validate, count new blocks
+    std::unordered_map<int64_t, std::pair<int32_t, int64_t>> sim;  // id -> (len, nblocks)
+    int64_t total = 0, new_blocks = 0;
+    for (int i = 0; i < nreq; ++i) {
+        auto it = p->requests.find(reqs[i]);
+        if (it == p->requests.end()) return fail(HALO_ENOENT, "unknown request %lld", (long long)reqs[i]);
+        if (ntok[i] < 0) return fail(HALO_EINVAL, "negative token count");
+        auto f = sim.find(reqs[i]);
+        if (f == sim.end())
+            f = sim.emplace(reqs[i], std::make_pair(it->second.len, (int64_t)it->second.blocks.size())).first;
+        const int64_t len = (int64_t)f->second.first + ntok[i];
+        if (len > INT32_MAX / 2) return fail(HALO_EINVAL, "suffix too long");
+        const int64_t need = ceil_div(len, kBlockTok);
+        if (need > f->second.second) {
+            new_blocks += need - f->second.second;
+            f->second.second = need;
+        }
+        f->second.first = (int32_t)len;
+        total += ntok[i];
+    }
+    if (total == 0) return HALO_OK;
+    if (!p->host_only && (!k || !v)) return fail(HALO_EINVAL, "null k/v");
+    DeviceGuard dg(p);
+    std::vector<int32_t> fresh;
+    halo_status st = alloc_blocks(p, new_blocks, fresh);
+    if (st != HALO_OK) return st;
+    // slot of every new token, in input order
+    std::unordered_map<int64_t, std::pair<int32_t, std::vector<int32_t>>> work;
+    std::vector<int32_t> slots;
+    slots.reserve(total);
+    size_t fi = 0;
+    for (int i = 0; i < nreq; ++i) {
+        auto w = work.find(reqs[i]);
+        if (w == work.end()) {
+            const Request &r = p->requests[reqs[i]];
+            w = work.emplace(reqs[i], std::make_pair(r.len, r.blocks)).first;
+        }
+        for (int32_t t = 0; t < ntok[i]; ++t) {
+            const int32_t pos = w->second.first++;
+            if (pos % kBlockTok == 0 && pos / kBlockTok >= (int32_t)w->second.second.size())
+                w->second.second.push_back(fresh[fi++]);
+            slots.push_back(w->second.second[pos / kBlockTok] * kBlockTok + pos % kBlockTok);
+        }
+    }
+    if (!p->host_only) {
+        cudaStream_t s = (cudaStream_t)stream;
+        const size_t bytes = (size_t)p->cfg.num_layers * total * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
+        Scratch ss, sk, sv;
+        const void *dk = nullptr, *dvp = nullptr;
+        st = upload(slots.data(), slots.size() * 4, s, ss);
+        if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
+        if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
+        if (st == HALO_OK) {
+            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, total, (const int32_t *)ss.ptr,
+                                              total, 0, 0, p->cfg.num_layers, p->num_sms, s);
+            if (e != cudaSuccess) st = fail(HALO_ECUDA, "scatter launch: %s", cudaGetErrorString(e));
+        }
+        if (st != HALO_OK) {
+            unalloc_blocks(p, fresh, 0);
+            return st;
+        }
+        note_stream(p, s);
+    }
+    for (auto &w : work) {
+        Request &r = p->requests[w.first];
+        r.len = w.second.first;
+        r.blocks = std::move(w.second.second);
+    }
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_suffix_truncate(halo_pool p, int32_t nreq, const int64_t *reqs, const int32_t *ntok) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (nreq < 0 || (nreq > 0 && (!reqs || !ntok))) return fail(HALO_EINVAL, "bad request list");
+    std::unordered_map<int64_t, int32_t> len;
+    for (int i = 0; i < nreq; ++i) {
+        auto it = p->requests.find(reqs[i]);
+        if (it == p->requests.end()) return fail(HALO_ENOENT, "unknown request %lld", (long long)reqs[i]);
+        auto f = len.emplace(reqs[i], it->second.len).first;
+        if (ntok[i] < 0 || ntok[i] > f->second) return fail(HALO_EINVAL, "truncate count out of range");
+        f->second -= ntok[i];
+    }
+    DeviceGuard dg(p);
+    for (auto &l : len) {
+        Request &r = p->requests[l.first];
+        r.len = l.second;
+        const size_t keep = (size_t)ceil_div(r.len, kBlockTok);
+        if (r.blocks.size() > keep) {
+            std::vector<int32_t> drop(r.blocks.begin() + keep, r.blocks.end());
+            r.blocks.resize(keep);
+            release_blocks(p, std::move(drop));
+        }
+    }
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_decode_plan(halo_pool p, int32_t nreq, const int64_t *reqs, const halo_plan_options *opt,
+                             void *stream, halo_plan *inout) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!inout || nreq < 1 || !reqs) return fail(HALO_EINVAL, "need nreq >= 1, reqs and a plan slot");
+    if (*inout && (*inout)->pool != p) return fail(HALO_EINVAL, "plan belongs to another pool");
+    if (opt && (opt->force_splits < 0)) return fail(HALO_EINVAL, "bad plan options");
+    DeviceGuard dg(p);
+    const bool fresh = *inout == nullptr;
+    halo_plan pl = fresh ? new halo_plan_s() : *inout;
+    pl->pool = p;
+    pl->opt = opt ? *opt : halo_plan_options{};
+    halo_status st = build_plan(pl, nreq, reqs);
+    if (st == HALO_OK) st = upload_plan(pl, (cudaStream_t)stream);
+    if (st != HALO_OK) {
+        if (fresh) {
+            if (pl->dbuf) cudaFree(pl->dbuf);
+            if (pl->part) cudaFree(pl->part);
+            delete pl;
+        }
+        return st;
+    }
+    if (fresh) {
+        p->plans_alive++;
+        *inout = pl;
+    }
+    note_stream(p, (cudaStream_t)stream);
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_decode_run(halo_plan pl, int32_t layer, const void *q, float *out, float *lse, float scale,
+                            void *stream) {
+    HALO_GUARD_BEGIN
+    if (!pl) return fail(HALO_EINVAL, "null plan");
+    halo_pool p = pl->pool;
+    if (p->host_only) return fail(HALO_EUNSUPPORTED, "compute on a host-only pool");
+    if (layer < 0 || layer >= p->cfg.num_layers) return fail(HALO_EINVAL, "layer out of range");
+    if (!q || !out) return fail(HALO_EINVAL, "null q/out");
+    if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)p->cfg.head_dim);
+    DeviceGuard dg(p);
+    return run_layer(pl, layer, q, out, lse, scale, (cudaStream_t)stream);
+    HALO_GUARD_END
+}
+
+halo_status halo_decode_run_stages(halo_plan pl, int32_t layer, int32_t mask, const void *q, float *out,
+                                   float *lse, float scale, void *stream) {
+    HALO_GUARD_BEGIN
+    if (!pl) return fail(HALO_EINVAL, "null plan");
+    halo_pool p = pl->pool;
+    if (p->host_only) return fail(HALO_EUNSUPPORTED, "compute on a host-only pool");
+    if (layer < 0 || layer >= p->cfg.num_layers) return fail(HALO_EINVAL, "layer out of range");
+    if (mask < 0 || mask > 3) return fail(HALO_EINVAL, "bad stage mask");
+    if (!q || ((mask & 2) && !out)) return fail(HALO_EINVAL, "null q/out");
+    if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)p->cfg.head_dim);
+    DeviceGuard dg(p);
+    return run_layer(pl, layer, q, out, lse, scale, (cudaStream_t)stream, mask);
+    HALO_GUARD_END
+}
+
+halo_status halo_decode_layers(halo_plan pl, int32_t nlayers, const void *q, float *out, float *lse, float scale,
+                               void *stream) {
+    HALO_GUARD_BEGIN
+    if (!pl) return fail(HALO_EINVAL, "null plan");
+    halo_pool p = pl->pool;
+    if (p->host_only) return fail(HALO_EUNSUPPORTED, "compute on a host-only pool");
+    if (nlayers < 1 || nlayers > p->cfg.num_layers) return fail(HALO_EINVAL, "nlayers out of range");
+    if (!q || !out) return fail(HALO_EINVAL, "null q/out");
+    if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)p->cfg.head_dim);
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t rows = (size_t)pl->nreq * p->cfg.num_q_heads;
+    const size_t q_layer = rows * p->cfg.head_dim;  // elements
+    const size_t o_layer = rows * p->cfg.head_dim;
+    const void *dq = q;
+    float *dout = out, *dlse = lse;
+    const bool q_host = !is_device_ptr(q), o_host = !is_device_ptr(out), l_host = lse && !is_device_ptr(lse);
+    auto grow = [&](void **buf, size_t *cap, size_t bytes) -> halo_status {
+        if (*cap >= bytes) return HALO_OK;
+        if (*buf) {
+            HALO_CUDA(cudaStreamSynchronize(s));
+            cudaFree(*buf);
+            *buf = nullptr;
+        }
+        HALO_CUDA(cudaMalloc(buf, bytes));
+        *cap = bytes;
+        return HALO_OK;
+    };
+    halo_status st;
+    if (q_host) {
+        if ((st = grow(&pl->q_stage, &pl->q_stage_cap, q_layer * nlayers * 2)) != HALO_OK) return st;
+        HALO_CUDA(cudaMemcpyAsync(pl->q_stage, q, q_layer * nlayers * 2, cudaMemcpyHostToDevice, s));
+        dq = pl->q_stage;
+    }
+    if (o_host) {
+        if ((st = grow((void **)&pl->o_stage, &pl->o_stage_cap, o_layer * nlayers * 4)) != HALO_OK) return st;
+        dout = pl->o_stage;
+    }
+    if (l_host) {
+        if ((st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * nlayers * 4)) != HALO_OK) return st;
+        dlse = pl->l_stage;
+    }
+    for (int l = 0; l < nlayers; ++l) {
+        st = run_layer(pl, l, static_cast<const uint16_t *>(dq) + q_layer * l, dout + o_layer * l,
+                       dlse ? dlse + rows * l : nullptr, scale, s);
+        if (st != HALO_OK) return st;
+    }
+    if (o_host) HALO_CUDA(cudaMemcpyAsync(out, dout, o_layer * nlayers * 4, cudaMemcpyDeviceToHost, s));
+    if (l_host) HALO_CUDA(cudaMemcpyAsync(lse, dlse, rows * nlayers * 4, cudaMemcpyDeviceToHost, s));
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_plan_get_info(halo_plan pl, halo_plan_info *info) {
+    if (!pl || !info) return fail(HALO_EINVAL, "null argument");
+    *info = pl->info;
+    return HALO_OK;
+}
+
+halo_status halo_plan_export(halo_plan pl, int32_t which, void *dst, int64_t cap, int64_t *n) {
+    if (!pl || !n) return fail(HALO_EINVAL, "null argument");
+    const void *src = nullptr;
+    int64_t cnt = 0;
+    switch (which) {
+        case 0: src = pl->req_order.data(); cnt = (int64_t)pl->req_order.size(); break;
+        case 1: src = pl->tiles.data(); cnt = (int64_t)pl->tiles.size() * 8; break;
+        case 2: src = pl->req_nslots.data(); cnt = (int64_t)pl->req_nslots.size(); break;
+        case 3: src = pl->unit_req.data(); cnt = (int64_t)pl->unit_req.size(); break;
+        case 4: src = pl->req_blk_off.data(); cnt = (int64_t)pl->req_blk_off.size(); break;
+        case 5: src = pl->req_blk.data(); cnt = (int64_t)pl->req_blk.size(); break;
+        default: return fail(HALO_EINVAL, "unknown export %d", which);
+    }
+    *n = cnt;
+    if (dst && cap > 0) memcpy(dst, src, (size_t)std::min(cap, cnt) * 4);
+    return HALO_OK;
+}
+
+halo_status halo_plan_destroy(halo_plan pl) {
+    HALO_GUARD_BEGIN
+    if (!pl) return fail(HALO_EINVAL, "null plan");
+    halo_pool p = pl->pool;
+    {
+        DeviceGuard dg(p);
+        if (pl->dbuf) cudaFree(pl->dbuf);
+        if (pl->part) cudaFree(pl->part);
+        if (pl->q_stage) cudaFree(pl->q_stage);
+        if (pl->o_stage) cudaFree(pl->o_stage);
+        if (pl->l_stage) cudaFree(pl->l_stage);
+    }
+    p->plans_alive--;
+    delete pl;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+// ------------------------------------------------------------------ migration
+halo_status halo_comm_unique_id(void *id_out) {
+    if (!id_out) return fail(HALO_EINVAL, "null id");
+    ncclUniqueId id;
+    HALO_NCCL(nccl().GetUniqueId(&id));
+    memcpy(id_out, &id, sizeof id);
+    return HALO_OK;
+}
+
+halo_status halo_comm_init(halo_pool p, const void *id, int32_t nranks, int32_t rank) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (p->host_only) return fail(HALO_EUNSUPPORTED, "host-only pool");
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(HALO_EINVAL, "bad communicator arguments");
+    if (p->comm) return fail(HALO_EBUSY, "communicator already initialised");
+    DeviceGuard dg(p);
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    HALO_NCCL(nccl().CommInitRank(&p->comm, nranks, uid, rank));
+    p->nranks = nranks;
+    p->rank = rank;
+    if (!p->side) HALO_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    for (auto &e : p->mig_ev)
+        if (!e) HALO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_migrate_send(halo_pool p, int64_t node, int32_t dst_rank, int32_t mode, void *stream) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!p->comm) return fail(HALO_ENCCL, "no communicator (halo_comm_init)");
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (dst_rank < 0 || dst_rank >= p->nranks || dst_rank == p->rank) return fail(HALO_EINVAL, "bad destination rank");
+    if (mode != 0 && mode != 1) return fail(HALO_EINVAL, "mode must be 0 (MOVE) or 1 (COPY)");
+    if (mode == 0 && (it->second.children || it->second.requests))
+        return fail(HALO_EBUSY, "MOVE of a referenced node");
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int32_t ntok = it->second.ntok;
+    const int L = p->cfg.num_layers, lpc = layers_per_chunk(p, ntok);
+    const size_t layer_bytes = (size_t)ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
+    const size_t chunk_bytes = 2 * lpc * layer_bytes;  // K then V
+    halo_status st = ensure_mig(p, 2 * chunk_bytes);
+    if (st != HALO_OK) return st;
+    std::vector<int32_t> slots = token_slots(it->second.blocks, ntok);
+    Scratch ss;
+    if ((st = upload(slots.data(), slots.size() * 4, s, ss)) != HALO_OK) return st;
+    cudaEvent_t *ev_packed = p->mig_ev, *ev_sent = p->mig_ev + 2;
+    int c = 0;
+    for (int l0 = 0; l0 < L; l0 += lpc, ++c) {
+        const int l1 = std::min(L, l0 + lpc), b = c & 1;
+        uint8_t *buf = static_cast<uint8_t *>(p->mig_buf) + b * chunk_bytes;
+        const size_t half = (size_t)(l1 - l0) * layer_bytes;
+        if (c >= 2) HALO_CUDA(cudaStreamWaitEvent(s, ev_sent[b], 0));
+        cudaError_t e = launch_kv_gather(p->geom, p->k, p->v, buf, buf + half, (const int32_t *)ss.ptr, ntok, l0,
+                                         l1, p->num_sms, s);
+        if (e != cudaSuccess) return fail(HALO_ECUDA, "pack launch: %s", cudaGetErrorString(e));
+        HALO_CUDA(cudaEventRecord(ev_packed[b], s));
+        HALO_CUDA(cudaStreamWaitEvent(p->side, ev_packed[b], 0));
+        HALO_NCCL(nccl().Send(buf, 2 * half, ncclUint8, dst_rank, p->comm, p->side));
+        HALO_CUDA(cudaEventRecord(ev_sent[b], p->side));
+    }
+    HALO_CUDA(cudaStreamWaitEvent(s, ev_sent[(c - 1) & 1], 0));
+    if (c >= 2) HALO_CUDA(cudaStreamWaitEvent(s, ev_sent[c & 1], 0));
+    note_stream(p, s);
+    if (mode == 0) {
+        const int64_t parent = it->second.parent;
+        release_blocks(p, std::move(it->second.blocks));
+        p->nodes.erase(it);
+        if (parent >= 0) p->nodes[parent].children--;
+    }
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_migrate_recv(halo_pool p, int32_t src_rank, int64_t parent, int32_t ntok, void *stream,
+                              int64_t *node_out) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!p->comm) return fail(HALO_ENCCL, "no communicator (halo_comm_init)");
+    if (!node_out || ntok < 1) return fail(HALO_EINVAL, "bad arguments");
+    if (src_rank < 0 || src_rank >= p->nranks || src_rank == p->rank) return fail(HALO_EINVAL, "bad source rank");
+    if (parent >= 0 && !p->nodes.count(parent)) return fail(HALO_ENOENT, "unknown parent %lld", (long long)parent);
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nblk = ceil_div(ntok, kBlockTok);
+    std::vector<int32_t> blocks;
+    halo_status st = alloc_blocks(p, nblk, blocks);
+    if (st != HALO_OK) return st;
+    const int L = p->cfg.num_layers, lpc = layers_per_chunk(p, ntok);
+    const size_t layer_bytes = (size_t)ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
+    const size_t chunk_bytes = 2 * lpc * layer_bytes;
+    if ((st = ensure_mig(p, 2 * chunk_bytes)) != HALO_OK) {
+        unalloc_blocks(p, blocks, 0);
+        return st;
+    }
+    std::vector<int32_t> slots = token_slots(blocks, nblk * kBlockTok);
+    Scratch ss;
+    if ((st = upload(slots.data(), slots.size() * 4, s, ss)) != HALO_OK) {
+        unalloc_blocks(p, blocks, 0);
+        return st;
+    }
+    cudaEvent_t *ev_recv = p->mig_ev, *ev_unpacked = p->mig_ev + 2;
+    HALO_CUDA(cudaEventRecord(ev_unpacked[0], s));
+    HALO_CUDA(cudaStreamWaitEvent(p->side, ev_unpacked[0], 0));
+    int c = 0;
+    for (int l0 = 0; l0 < L; l0 += lpc, ++c) {
+        const int l1 = std::min(L, l0 + lpc), b = c & 1;
+        uint8_t *buf = static_cast<uint8_t *>(p->mig_buf) + b * chunk_bytes;
+        const size_t half = (size_t)(l1 - l0) * layer_bytes;
+        if (c >= 2) HALO_CUDA(cudaStreamWaitEvent(p->side, ev_unpacked[b], 0));
+        HALO_NCCL(nccl().Recv(buf, 2 * half, ncclUint8, src_rank, p->comm, p->side));
+        HALO_CUDA(cudaEventRecord(ev_recv[b], p->side));
+        HALO_CUDA(cudaStreamWaitEvent(s, ev_recv[b], 0));
+        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, buf, buf + half, ntok, (const int32_t *)ss.ptr, ntok,
+                                          nblk * kBlockTok - ntok, l0, l1, p->num_sms, s);
+        if (e != cudaSuccess) return fail(HALO_ECUDA, "unpack launch: %s", cudaGetErrorString(e));
+        HALO_CUDA(cudaEventRecord(ev_unpacked[b], s));
+    }
+    note_stream(p, s);
+    const int64_t id = p->next_id++;
+    Node n;
+    n.parent = parent;
+    n.ntok = ntok;
+    n.blocks = std::move(blocks);
+    p->nodes.emplace(id, std::move(n));
+    if (parent >= 0) p->nodes[parent].children++;
+    *node_out = id;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_t parent_dst, void *stream,
+                              int64_t *node_out) {
+    HALO_GUARD_BEGIN
+    if (check_pool(src) || check_pool(dst)) return HALO_EINVAL;
+    if (src->host_only || dst->host_only) return fail(HALO_EUNSUPPORTED, "host-only pool");
+    if (src->cfg.device != dst->cfg.device || src->cfg.num_layers != dst->cfg.num_layers ||
+        src->cfg.num_kv_heads != dst->cfg.num_kv_heads || src->cfg.head_dim != dst->cfg.head_dim)
+        return fail(HALO_EINVAL, "pools differ in device or KV geometry");
+    auto it = src->nodes.find(node);
+    if (it == src->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (!node_out) return fail(HALO_EINVAL, "null node_out");
+    if (parent_dst >= 0 && !dst->nodes.count(parent_dst))
+        return fail(HALO_ENOENT, "unknown parent %lld", (long long)parent_dst);
+    DeviceGuard dg(src);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int32_t ntok = it->second.ntok;
+    const int64_t nblk = ceil_div(ntok, kBlockTok);
+    std::vector<int32_t> blocks;
+    halo_status st = alloc_blocks(dst, nblk, blocks);
+    if (st != HALO_OK) return st;
+    const int L = src->cfg.num_layers, lpc = layers_per_chunk(src, ntok);
+    const size_t layer_bytes = (size_t)ntok * src->cfg.num_kv_heads * src->cfg.head_dim * 2;
+    std::vector<int32_t> sslots = token_slots(it->second.blocks, ntok);
+    std::vector<int32_t> dslots = token_slots(blocks, nblk * kBlockTok);
+    Scratch s1, s2, buf;
+    if ((st = upload(sslots.data(), sslots.size() * 4, s, s1)) == HALO_OK &&
+        (st = upload(dslots.data(), dslots.size() * 4, s, s2)) == HALO_OK) {
+        buf.s = s;
+        if (cudaMallocAsync(&buf.ptr, 2 * lpc * layer_bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            st = fail(HALO_ENOMEM, "staging allocation failed");
+        }
+    }
+    for (int l0 = 0; st == HALO_OK && l0 < L; l0 += lpc) {
+        const int l1 = std::min(L, l0 + lpc);
+        uint8_t *b = static_cast<uint8_t *>(buf.ptr);
+        const size_t half = (size_t)(l1 - l0) * layer_bytes;
+        cudaError_t e = launch_kv_gather(src->geom, src->k, src->v, b, b + half, (const int32_t *)s1.ptr, ntok, l0, l1,
+                                         src->num_sms, s);
+        if (e == cudaSuccess)
+            e = launch_kv_scatter(dst->geom, dst->k, dst->v, b, b + half, ntok, (const int32_t *)s2.ptr, ntok,
+                                  nblk * kBlockTok - ntok, l0, l1, dst->num_sms, s);
+        if (e != cudaSuccess) st = fail(HALO_ECUDA, "clone launch: %s", cudaGetErrorString(e));
+    }
+    if (st != HALO_OK) {
+        unalloc_blocks(dst, blocks, 0);
+        return st;
+    }
+    note_stream(src, s);
+    note_stream(dst, s);
+    const int64_t id = dst->next_id++;
+    Node n;
+    n.parent = parent_dst;
+    n.ntok = ntok;
+    n.blocks = std::move(blocks);
+    dst->nodes.emplace(id, std::move(n));
+    if (parent_dst >= 0) dst->nodes[parent_dst].children++;
+    *node_out = id;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+}  // extern "C"

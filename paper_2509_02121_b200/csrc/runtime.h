@@ -1,0 +1,92 @@
+// Host runtime state of libhalo_attn (pool, prefix tree, requests, plans).  Private.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/halo_attn.h"
+#include "halo_internal.h"
+
+typedef struct ncclComm *ncclComm_t;
+
+namespace halo {
+
+struct Node {
+    int64_t parent = -1;
+    int32_t ntok = 0;
+    std::vector<int32_t> blocks;
+    int32_t children = 0;
+    int32_t requests = 0;
+};
+
+struct Request {
+    int64_t leaf = -1;
+    int32_t len = 0;  // suffix tokens
+    std::vector<int32_t> blocks;
+};
+
+struct PendingFree {
+    std::vector<cudaEvent_t> events;
+    std::vector<int32_t> blocks;
+};
+
+struct StreamFence {
+    cudaStream_t stream;
+    uint64_t last_use;
+};
+
+}  // namespace halo
+
+struct halo_pool_s {
+    halo_pool_config cfg{};
+    halo::PoolGeom geom{};
+    bool host_only = false;
+    int num_sms = 148;
+    void *k = nullptr, *v = nullptr;
+    bool own_storage = false;
+    std::vector<int32_t> free_list;  // stack: back() is the next block handed out
+    std::vector<halo::PendingFree> pending;
+    std::vector<cudaEvent_t> event_cache;
+    std::vector<halo::StreamFence> streams;  // streams that enqueued work on this pool
+    uint64_t use_clock = 0;
+    std::unordered_map<int64_t, halo::Node> nodes;
+    std::unordered_map<int64_t, halo::Request> requests;
+    int64_t next_id = 1;
+    int32_t plans_alive = 0;
+    CUtensorMap tmap_k{}, tmap_v{};
+    // migration
+    ncclComm_t comm = nullptr;
+    int32_t nranks = 0, rank = -1;
+    cudaStream_t side = nullptr;
+    void *mig_buf = nullptr;
+    size_t mig_cap = 0;
+    cudaEvent_t mig_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+struct halo_plan_s {
+    halo_pool pool = nullptr;
+    int32_t nreq = 0;
+    halo_plan_options opt{};
+    std::vector<int32_t> req_order, node_blocks, unit_req, req_blk_off, req_nslots;
+    std::vector<uint32_t> req_blk;
+    std::vector<halo::PrefixTile> tiles;
+    halo_plan_info info{};
+    std::vector<uint8_t> host_buf;
+    void *dbuf = nullptr;
+    size_t dbuf_cap = 0;
+    float *part = nullptr;
+    size_t part_cap = 0;
+    halo::PlanDev dev{};
+    // staging for halo_decode_layers with host buffers
+    void *q_stage = nullptr;
+    size_t q_stage_cap = 0;
+    float *o_stage = nullptr;
+    size_t o_stage_cap = 0;
+    float *l_stage = nullptr;
+    size_t l_stage_cap = 0;
+};

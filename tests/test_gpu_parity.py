@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle, element by element.
+
+Bar (north_star): max |out_gpu - o_oracle| <= 2e-3 on the fp32 output (bf16 KV inputs,
+fp32 accumulation); max |lse_gpu - lse_oracle| <= 1e-3.  Migrated / cloned
+blocks must be bit-exact; permutations and reruns bit-identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2509_02121_b200 as halo
+from paper_2509_02121_b200 import build as halo_build
+from paper_2509_02121_b200.abi import PlanOptions
+from paper_2509_02121_b200.loader import append_step, load
+from synth import make_config
+from synth.gen import bf16_bits
+
+pytestmark = pytest.mark.gpu
+
+OUT_TOL = 2e-3
+LSE_TOL = 1e-3
+DEV = 0
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    halo_build.build()
+    halo.load_library()
+    torch.cuda.set_device(DEV)
+
+
+def run_step(wl, opt=None, layers=None, reqs_perm=None):
+    ld = load(wl, DEV)
+    append_step(ld, wl, 0, DEV)
+    order = list(range(wl.nreq)) if reqs_perm is None else list(reqs_perm)
+    plan = ld.pool.plan([ld.req_ids[i] for i in order], opt)
+    q = wl.q(0, f"cuda:{DEV}")[:, order].contiguous()
+    L = wl.layers
+    out = torch.full((L, len(order), wl.hq, wl.d), float("nan"), device=f"cuda:{DEV}")
+    lse = torch.full((L, len(order), wl.hq), float("nan"), device=f"cuda:{DEV}")
+    for l in (layers if layers is not None else range(L)):
+        plan.run(l, q[l], out[l], lse[l])
+    torch.cuda.synchronize()
+    return ld, plan, out.cpu().numpy(), lse.cpu().numpy()
+
+
+def cleanup(ld, plan):
+    plan.destroy()
+    ld.pool.destroy()
+
+
+def check(wl, opt=None, layers=None, sample=None):
+    layers = list(range(wl.layers)) if layers is None else layers
+    ld, plan, out, lse = run_step(wl, opt, layers)
+    info = plan.info()
+    reqs = list(range(wl.nreq)) if sample is None else sample
+    worst_o = worst_l = 0.0
+    for l in layers:
+        ro, rl = oracle.decode_reference(wl, l, steps=1, requests=reqs)
+        eo = np.abs(out[l][reqs] - ro).max()
+        el = np.abs(lse[l][reqs] - rl).max()
+        worst_o, worst_l = max(worst_o, eo), max(worst_l, el)
+    cleanup(ld, plan)
+    assert np.isfinite(worst_o) and worst_o <= OUT_TOL, (worst_o, info)
+    assert np.isfinite(worst_l) and worst_l <= LSE_TOL, (worst_l, info)
+    return info, worst_o, worst_l
+
+
+def opts(min_rows=0, splits=0, max_splits=0):
+    return PlanOptions(min_rows, splits, max_splits, 0)
+
+
+def test_toy_c0_folded():
+    info, *_ = check(make_config("toy"))
+    assert info["tensor_nodes"] == 0 and info["folded_nodes"] == 1
+
+
+def test_toy_c0_tensor_path_d64_g1():
+    info, *_ = check(make_config("toy"), opts(min_rows=1))
+    assert info["tensor_nodes"] == 1 and info["k1_tiles"] == 1
+
+
+@pytest.mark.parametrize("min_rows,splits", [(1, 0), (1, 3), (16, 2), (0, 0), (100000, 0)])
+def test_ragged_tree(min_rows, splits):
+    """depth-3 tree, partial blocks, no-prefix requests, 0-token initial suffixes, g=4."""
+    check(make_config("ragged"), opts(min_rows, splits))
+
+
+def test_fanout_small_k1_multi_mtile():
+    wl = make_config("fanout", layers=2, nreq=80, prefix=1000, suffix=40)
+    info, *_ = check(wl)
+    assert info["tensor_nodes"] == 1 and info["k1_tiles"] >= 24
+
+
+def test_tree_two_levels():
+    wl = make_config("tree", layers=2, root=700, roles=4, role_tok=300, per_role=40, suffix=20)
+    info, *_ = check(wl)
+    assert info["tensor_nodes"] == 5 and info["max_slots"] >= 2
+
+
+def test_ragged_suffix_lengths():
+    check(make_config("ragged_suffix", layers=1, nreq=40, prefix=512))
+
+
+@pytest.mark.parametrize("alpha", [2.0])
+def test_sharper_scores(alpha):
+    check(make_config("fanout", layers=1, nreq=64, prefix=600, suffix=30, alpha_q=alpha))
+
+
+def test_d64_g2():
+    check(make_config("fanout", layers=1, nreq=70, prefix=333, suffix=17, hq=4, hkv=2, d=64))
+
+
+def test_g8_and_g1():
+    check(make_config("fanout", layers=1, nreq=40, prefix=260, suffix=9, hq=16, hkv=2))
+    check(make_config("fanout", layers=1, nreq=130, prefix=260, suffix=9, hq=4, hkv=4),
+          opts(min_rows=1))
+
+
+def test_full_c1_sampled_at_bench_configuration():
+    """C1 (BASELINE configs[1]) at full size: 256 requests, 2k prefix, 32 layers; sampled
+    requests at the first and last layer vs the oracle (the launch configuration bench.py
+    times: default plan)."""
+    wl = make_config("fanout")
+    sample = [0, 1, 77, 128, 200, 255]
+    check(wl, layers=[0, 31], sample=sample)
+
+
+def test_request_permutation_and_rerun_are_bit_identical():
+    wl = make_config("ragged")
+    ld, plan, out, lse = run_step(wl, opts(min_rows=1, splits=2))
+    # rerun the same plan
+    q = wl.q(0, f"cuda:{DEV}")
+    out2 = torch.empty((wl.nreq, wl.hq, wl.d), device=f"cuda:{DEV}")
+    lse2 = torch.empty((wl.nreq, wl.hq), device=f"cuda:{DEV}")
+    plan.run(1, q[1], out2, lse2)
+    torch.cuda.synchronize()
+    assert np.array_equal(out2.cpu().numpy(), out[1]) and np.array_equal(lse2.cpu().numpy(), lse[1])
+    cleanup(ld, plan)
+    perm = np.random.Generator(np.random.PCG64(5)).permutation(wl.nreq)
+    ld, plan, outp, lsep = run_step(wl, opts(min_rows=1, splits=2), reqs_perm=perm)
+    assert np.array_equal(outp, out[:, perm]) and np.array_equal(lsep, lse[:, perm])
+    cleanup(ld, plan)
+
+
+def test_physical_block_placement_is_bit_invisible():
+    wl = make_config("tree", layers=1, root=300, roles=3, role_tok=100, per_role=30, suffix=40)
+    ld, plan, out, lse = run_step(wl)
+    cleanup(ld, plan)
+    # same logical content, different physical blocks: fragment the pool first
+    pool = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, 4000, DEV)
+    junk = [pool.register_prefix(-1, 16 * (i % 3 + 1),
+                                 *[torch.zeros(wl.layers, 16 * (i % 3 + 1), wl.hkv, wl.d,
+                                               dtype=torch.bfloat16, device="cuda")] * 2)
+            for i in range(40)]
+    for j in junk[::2]:
+        pool.release_prefix(j)
+    torch.cuda.synchronize()
+    ld2 = load(wl, DEV, pool=pool)
+    append_step(ld2, wl, 0, DEV)
+    plan2 = pool.plan(ld2.req_ids)
+    q = wl.q(0, "cuda")
+    out2 = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda")
+    lse2 = torch.empty((wl.nreq, wl.hq), device="cuda")
+    plan2.run(0, q[0], out2, lse2)
+    torch.cuda.synchronize()
+    assert np.array_equal(out2.cpu().numpy(), out[0]) and np.array_equal(lse2.cpu().numpy(), lse[0])
+    plan2.destroy()
+    pool.destroy()
+
+
+def test_prefix_read_returns_registered_tensors():
+    wl = make_config("ragged", layers=3)
+    ld = load(wl, DEV)
+    for n in wl.nodes:
+        k, v = wl.node_kv(n.ident, "cuda")
+        ko, vo = torch.empty_like(k), torch.empty_like(v)
+        ld.pool.read_prefix(ld.node_ids[n.ident], ko, vo)
+        torch.cuda.synchronize()
+        assert torch.equal(ko.view(torch.int16), k.view(torch.int16))
+        assert torch.equal(vo.view(torch.int16), v.view(torch.int16))
+    ld.pool.destroy()
+
+
+def test_clone_is_bit_exact_and_decodes_identically():
+    """K4 pack/unpack relocation (the migration data path without NCCL)."""
+    wl = make_config("fanout", layers=3, nreq=40, prefix=777, suffix=5)
+    ld = load(wl, DEV)
+    src = ld.node_ids[0]
+    dst_pool = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, 1000, DEV)
+    new = ld.pool.clone_prefix(src, dst_pool, -1)
+    k, v = wl.node_kv(0, "cuda")
+    ko, vo = torch.empty_like(k), torch.empty_like(v)
+    dst_pool.read_prefix(new, ko, vo)
+    torch.cuda.synchronize()
+    assert torch.equal(ko.view(torch.int16), k.view(torch.int16))
+    assert torch.equal(vo.view(torch.int16), v.view(torch.int16))
+    # decode the same requests against the clone: bit-identical outputs
+    append_step(ld, wl, 0, DEV)
+    plan = ld.pool.plan(ld.req_ids)
+    q = wl.q(0, "cuda")
+    o1 = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda")
+    plan.run(2, q[2], o1)
+    reqs2 = [dst_pool.open_request(new) for _ in range(wl.nreq)]
+    sk, sv = wl.suffix_kv("cuda")
+    dst_pool.append(reqs2, [r.suffix for r in wl.requests], sk, sv)
+    nk, nv = wl.new_kv(0, "cuda")
+    dst_pool.append(reqs2, [1] * wl.nreq, nk, nv)
+    plan2 = dst_pool.plan(reqs2)
+    o2 = torch.empty_like(o1)
+    plan2.run(2, q[2], o2)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    plan.destroy()
+    plan2.destroy()
+    dst_pool.destroy()
+    ld.pool.destroy()
+
+
+def test_decode_layers_with_host_buffers_matches_device_path():
+    wl = make_config("fanout", layers=2, nreq=64, prefix=300, suffix=10)
+    ld = load(wl, DEV)
+    append_step(ld, wl, 0, DEV)
+    plan = ld.pool.plan(ld.req_ids)
+    q = wl.q(0, "cuda")
+    od = torch.empty((2, wl.nreq, wl.hq, wl.d), device="cuda")
+    ld_ = torch.empty((2, wl.nreq, wl.hq), device="cuda")
+    plan.run_layers(2, q, od, ld_)
+    qh = q.cpu().pin_memory()
+    oh = torch.empty((2, wl.nreq, wl.hq, wl.d)).pin_memory()
+    lh = torch.empty((2, wl.nreq, wl.hq)).pin_memory()
+    plan.run_layers(2, qh, oh, lh)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, od.cpu()) and torch.equal(lh, ld_.cpu())
+    plan.destroy()
+    ld.pool.destroy()
+
+
+def test_truncate_then_append_is_a_stationary_step():
+    """The bench keeps the batch stationary: roll back the decoded token, append again."""
+    wl = make_config("fanout", layers=1, nreq=64, prefix=256, suffix=31)
+    ld, plan, out, lse = run_step(wl)
+    ld.pool.truncate(ld.req_ids, [1] * wl.nreq)
+    append_step(ld, wl, 0, DEV)
+    plan = ld.pool.plan(ld.req_ids, reuse=plan)
+    q = wl.q(0, "cuda")
+    o2 = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda")
+    plan.run(0, q[0], o2)
+    torch.cuda.synchronize()
+    assert np.array_equal(o2.cpu().numpy(), out[0])
+    cleanup(ld, plan)

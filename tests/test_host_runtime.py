@@ -1,0 +1,207 @@
+"""CPU tests of the C-ABI library: symbol exports, and the host logic (block allocator,
+prefix tree, requests, decode planner) on a host-only pool (device = -1: bookkeeping only,
+no device memory and no kernels -- compute calls return HALO_EUNSUPPORTED)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2509_02121_b200 as halo
+from paper_2509_02121_b200.abi import SIGNATURES, PlanOptions
+from paper_2509_02121_b200 import build as halo_build
+from synth import make_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    halo_build.build()
+    halo.load_library()
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "halo_attn.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(halo_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(halo.lib_path())
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(SIGNATURES), set(syms) ^ set(SIGNATURES)
+    assert lib.halo_abi_version() == 1
+
+
+def host_pool(layers=2, hkv=2, hq=8, d=128, cap=1000):
+    return halo.Pool(layers, hkv, hq, d, cap, device=-1)
+
+
+def test_pool_config_validation():
+    for kw in [dict(hkv=3, hq=8), dict(d=96), dict(hkv=1, hq=16), dict(cap=0)]:
+        with pytest.raises(halo.HaloError) as e:
+            host_pool(**kw)
+        assert e.value.name == "HALO_EINVAL"
+
+
+def test_allocator_accounting_and_enomem_is_clean():
+    p = host_pool(cap=10)
+    assert p.stats() == (10, 0)
+    a = p.register_prefix(-1, 33)  # 3 blocks
+    assert p.stats() == (7, 3)
+    r = p.open_request(a)
+    p.append([r], [16 * 7])  # 7 blocks -> pool full
+    assert p.stats() == (0, 10)
+    with pytest.raises(halo.HaloError) as e:
+        p.append([r], [1])
+    assert e.value.name == "HALO_ENOMEM"
+    assert p.request_info(r)["suffix_len"] == 112 and p.stats() == (0, 10)
+    with pytest.raises(halo.HaloError):
+        p.register_prefix(-1, 1)
+    p.truncate([r], [17])
+    assert p.request_info(r) == {"leaf": a, "suffix_len": 95, "nblocks": 6}
+    assert p.stats() == (1, 9)
+    p.close_request(r)
+    assert p.stats() == (7, 3)
+    p.release_prefix(a)
+    assert p.stats() == (10, 0)
+    p.destroy()
+
+
+def test_tree_refcounts_and_errors():
+    p = host_pool()
+    root = p.register_prefix(-1, 40)
+    child = p.register_prefix(root, 20)
+    r = p.open_request(child)
+    with pytest.raises(halo.HaloError) as e:
+        p.release_prefix(root)
+    assert e.value.name == "HALO_EBUSY"
+    with pytest.raises(halo.HaloError) as e:
+        p.release_prefix(child)
+    assert e.value.name == "HALO_EBUSY"
+    with pytest.raises(halo.HaloError) as e:
+        p.open_request(12345)
+    assert e.value.name == "HALO_ENOENT"
+    with pytest.raises(halo.HaloError) as e:
+        p.register_prefix(999, 5)
+    assert e.value.name == "HALO_ENOENT"
+    info = p.node_info(child)
+    assert info["parent"] == root and info["ntok"] == 20 and len(info["blocks"]) == 2
+    p.close_request(r)
+    p.release_prefix(child)
+    p.release_prefix(root)
+    ids = {root, child, r}
+    assert len(ids) == 3  # ids are unique across kinds
+    p.destroy()
+
+
+def test_append_handles_repeated_ids_and_fresh_suffix_blocks():
+    p = host_pool()
+    n = p.register_prefix(-1, 7)  # partial block: the suffix must start in a fresh block
+    r = p.open_request(n)
+    p.append([r, r, r], [5, 11, 1])
+    inf = p.request_info(r)
+    assert inf["suffix_len"] == 17 and inf["nblocks"] == 2
+    assert p.stats()[1] == 3
+
+
+def plan_of(wl, **opt):
+    p = host_pool(wl.layers, wl.hkv, wl.hq, wl.d, cap=100000)
+    from paper_2509_02121_b200.loader import load
+    ld = load(wl, device=-1, pool=p)
+    reqs = ld.req_ids
+    # one decode step appends a token to each request
+    p.append(reqs, [1] * len(reqs))
+    o = PlanOptions(opt.get("min_rows", 0), opt.get("force_splits", 0), opt.get("max_splits", 0), 0)
+    return p, ld, p.plan(reqs, o)
+
+
+def test_plan_dfs_ranges_are_contiguous_and_tiles_cover_every_row_token_once():
+    wl = make_config("ragged")
+    for min_rows, fs in [(1, 0), (1, 3), (64, 0), (16, 2)]:
+        p, ld, pl = plan_of(wl, min_rows=min_rows, force_splits=fs)
+        order = pl.export("req_order")
+        assert sorted(order) == list(range(wl.nreq))
+        # requests under any node are contiguous in DFS order
+        pos = {int(r): i for i, r in enumerate(order)}
+        for n in wl.nodes:
+            under = [i for i in range(wl.nreq) if n.ident in wl.path(i)]
+            if under:
+                ps = sorted(pos[i] for i in under)
+                assert ps == list(range(ps[0], ps[0] + len(ps)))
+        tiles = pl.export("tiles")
+        g = wl.g
+        covered = {}
+        for (req_off, nrows, head, t0, t1, blk_off, slot, node) in tiles:
+            assert 0 < nrows <= 128 and t0 % 128 == 0 and t1 > t0
+            for row in range(nrows):
+                r = int(order[req_off + row // g])
+                for t in sorted({int(t0), int(t1) - 1}):
+                    key = (r, head * g + row % g, int(slot), t)
+                    assert key not in covered
+                    covered[key] = True
+        nslots = pl.export("req_nslots")
+        info = pl.info()
+        assert info["max_slots"] == (max(nslots) if len(nslots) else 0)
+        # K2 blocks per request = folded nodes' blocks + suffix blocks, counts add up
+        off = pl.export("req_blk_off")
+        blk = pl.export("req_blk")
+        slot_tokens = {}
+        for (req_off, nrows, head, t0, t1, blk_off, slot, node) in tiles:
+            for row in range(nrows):
+                r = int(order[req_off + row // g])
+                slot_tokens[(r, int(slot))] = slot_tokens.get((r, int(slot)), 0) + 0
+        for i in range(wl.nreq):
+            cnt = sum(int((e >> 27) + 1) for e in blk[off[i]:off[i + 1]])
+            k1_tok = 0
+            for (req_off, nrows, head, t0, t1, blk_off, slot, node) in tiles:
+                if head != 0:
+                    continue
+                rows_req = {int(order[req_off + row // g]) for row in range(nrows)}
+                if i in rows_req:
+                    k1_tok += t1 - t0
+            assert cnt + k1_tok == wl.context_len(i, steps=1), (i, cnt, k1_tok)
+            assert nslots[i] <= info["max_slots"]
+        pl.destroy()
+        p.destroy()
+
+
+def test_plan_rejects_empty_context_and_unknown_ids():
+    p = host_pool()
+    r = p.open_request(-1)
+    with pytest.raises(halo.HaloError) as e:
+        p.plan([r])
+    assert e.value.name == "HALO_EINVAL"
+    with pytest.raises(halo.HaloError) as e:
+        p.plan([777])
+    assert e.value.name == "HALO_ENOENT"
+
+
+def test_plan_split_choice_fills_the_sms():
+    wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=15)
+    p, ld, pl = plan_of(wl)
+    info = pl.info()
+    assert info["tensor_nodes"] == 1 and info["folded_nodes"] == 0
+    assert 100 <= info["k1_tiles"] <= 296
+    assert info["k1_flops"] == 4.0 * 256 * 4 * 2048 * 128 * 8
+    # compute on a host-only pool is refused, not emulated
+    with pytest.raises(halo.HaloError) as e:
+        pl.run(0, 1, 1)
+    assert e.value.name == "HALO_EUNSUPPORTED"
+    with pytest.raises(halo.HaloError):
+        p.destroy()  # plan still alive -> EBUSY
+    pl.destroy()
+    p.destroy()
+
+
+def test_plan_rebuild_in_place():
+    wl = make_config("ragged")
+    p, ld, pl = plan_of(wl, min_rows=1)
+    pl2 = p.plan(ld.req_ids[:5], reuse=pl)
+    assert pl2 is pl and pl.info()["nreq"] == 5
+    pl.destroy()

@@ -123,16 +123,19 @@ def cpu_model():
 
 
 # ------------------------------------------------------------------ oracle (CPU) legs
-def oracle_sample(wl, budget_s: float, max_requests: int = 64, layer: int = 0):
+def oracle_sample(wl, budget_s: float, max_queries: int = 100000):
     """Time the fp64 oracle (as it stands) on a bounded sample of the same workload:
-    requests of `layer` after one decode step, contexts gathered outside the timer."""
+    (request, layer) queries in order, contexts gathered outside the timer, until
+    `budget_s` seconds of oracle compute."""
     import numpy as np
     import oracle
     nthreads = host_cores()
     scale = 1.0 / np.sqrt(wl.d)
     t_total, done = 0.0, 0
-    for r in range(min(wl.nreq, max_requests)):
-        k, v = oracle.request_context(wl, r, layer, steps=1)
+    cache = {}
+    for i in range(min(wl.nreq * wl.layers, max_queries)):
+        layer, r = divmod(i, wl.nreq)
+        k, v = oracle.request_context(wl, r, layer, steps=1, cache=cache)
         qb = oracle._bits(wl.q(0, "cpu", layer, request=r))
         t0 = time.perf_counter()
         oracle.attend(qb, k, v, scale, nthreads)
@@ -225,14 +228,15 @@ def main():
     lse = torch.empty((L, R, Hq), device=f"cuda:{dev}")
     ones = [1] * R
     pool.append(reqs, ones, nk, nv)
-    plan = pool.plan(reqs)
+    popt = halo.PlanOptions(0, 0, 0, int(os.environ.get("HALO_K2_CHUNK", "0")))
+    plan = pool.plan(reqs, popt)
     info = plan.info()
     stream = torch.cuda.current_stream()
 
     def step(evs=None):
         pool.truncate(reqs, ones)                 # stationary batch: roll back, re-append
         pool.append(reqs, ones, nk, nv)
-        pool.plan(reqs, reuse=plan)
+        pool.plan(reqs, popt, reuse=plan)
         for l in range(L):
             if evs is not None:
                 evs[l][0].record(stream)
@@ -292,7 +296,7 @@ def main():
         def e2e_step():
             pool.truncate(reqs, ones)
             pool.append(reqs, ones, nk_h, nv_h)
-            pool.plan(reqs, reuse=plan)
+            pool.plan(reqs, popt, reuse=plan)
             plan.run_layers(L, q_h, out_h)
         for _ in range(3):
             e2e_step()
@@ -321,9 +325,9 @@ def main():
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         n, t, cores = oracle_sample(wl, args.cpu_budget)
         extra["cpu_baseline"] = {"value": n / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                 "sample": f"{n} requests of C1 at layer 0 (unshared fp64 "
-                                           f"attention over 2304 tokens x 32 heads), "
-                                           f"{t:.1f} s", "cpu_model": cpu_model()}
+                                 "sample": f"first {n} (request, layer) queries of C1 (unshared "
+                                           f"fp64 attention over 2304 tokens x 32 heads each), "
+                                           f"{t:.1f} s of oracle time", "cpu_model": cpu_model()}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

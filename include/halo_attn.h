@@ -146,7 +146,7 @@ typedef struct {
     int32_t force_splits;    /* > 0: split every K1 node's tokens into this many ranges
                                 (tests); 0: the plan chooses (fills the 148 SMs).      */
     int32_t max_splits;      /* cap on splits per node; <= 0: default 16                */
-    int32_t reserved;
+    int32_t k2_chunk_blocks; /* K2 work-queue chunk in 16-token blocks; <= 0: plan chooses */
 } halo_plan_options;
 
 /* Build (or rebuild in place, when *inout != NULL) the plan of one decode step for the
@@ -197,7 +197,10 @@ halo_status halo_plan_get_info(halo_plan plan, halo_plan_info *info);
  * caller indices), 1 K1 tiles (int32 x 8 each: req_off, nrows, kv_head, tok_begin,
  * tok_end, blk_off, slot, node_index), 2 per-request slot counts (int32), 3 K2 request
  * order (int32), 4 per-request K2 block CSR offsets (int32, nreq+1), 5 K2 block entries
- * (uint32: block | (ntok-1) << 27).  *n receives the element count; copies at most cap. */
+ * (uint32: block | (ntok-1) << 27), and the K2 schedule: 6 unit block offsets (nunits+1),
+ * 7/8 first/end unit of each chunk, 9 pieces per unit, 10 chunk block bounds (nchunks+1),
+ * all int32.  *n receives the element count; copies at
+ * most cap. */
 halo_status halo_plan_export(halo_plan plan, int32_t which, void *dst, int64_t cap,
                              int64_t *n);
 halo_status halo_plan_destroy(halo_plan plan);

@@ -94,14 +94,22 @@ def _bits(t) -> np.ndarray:
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
 
 
-def request_context(wl, r: int, layer: int, steps: int = 1):
+def request_context(wl, r: int, layer: int, steps: int = 1, cache: dict | None = None):
     """(k_bits, v_bits) [T][Hkv][d] for request r at `layer` after `steps` decode steps:
-    prefix path root -> leaf, then the initial suffix, then the appended tokens."""
+    prefix path root -> leaf, then the initial suffix, then the appended tokens.
+    `cache` (optional) memoises the generated prefix-node tensors across requests."""
     ks, vs = [], []
     for n in wl.path(r):
-        k, v = wl.node_kv(n, "cpu", layer)
-        ks.append(_bits(k))
-        vs.append(_bits(v))
+        key = (n, layer)
+        if cache is not None and key in cache:
+            k, v = cache[key]
+        else:
+            k, v = wl.node_kv(n, "cpu", layer)
+            k, v = _bits(k), _bits(v)
+            if cache is not None:
+                cache[key] = (k, v)
+        ks.append(k)
+        vs.append(v)
     k, v = wl.suffix_kv("cpu", layer, request=r)
     ks.append(_bits(k))
     vs.append(_bits(v))
@@ -122,8 +130,9 @@ def decode_reference(wl, layer: int, steps: int = 1, requests=None, scale=None,
         scale = 1.0 / np.sqrt(wl.d)
     out = np.empty((len(requests), wl.hq, wl.d), dtype=np.float64)
     lse = np.empty((len(requests), wl.hq), dtype=np.float64)
+    cache = {}
     for i, r in enumerate(requests):
-        k, v = request_context(wl, r, layer, steps)
+        k, v = request_context(wl, r, layer, steps, cache)
         q = _bits(wl.q(steps - 1, "cpu", layer, request=r))
         out[i], lse[i] = attend(q, k, v, scale, nthreads)
     return out, lse

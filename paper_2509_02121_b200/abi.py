@@ -29,7 +29,7 @@ class PoolConfig(C.Structure):
 
 class PlanOptions(C.Structure):
     _fields_ = [("min_tensor_rows", _i32), ("force_splits", _i32), ("max_splits", _i32),
-                ("reserved", _i32)]
+                ("k2_chunk_blocks", _i32)]
 
 
 class PlanInfo(C.Structure):
@@ -75,17 +75,19 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _LIB_PATH
+    # HALO_LIB selects a debug build of the same library (e.g. libhalo_attn_trace.so)
+    return os.environ.get("HALO_LIB", _LIB_PATH)
 
 
 def load_library():
     """Load libhalo_attn.so (raises if it was not built: there is no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise ImportError(f"{_LIB_PATH} is missing: build it with "
+        path = lib_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with "
                               "`python -m paper_2509_02121_b200.build` (no CPU fallback exists)")
-        lib = C.CDLL(_LIB_PATH)
+        lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
@@ -268,7 +270,8 @@ class Pool:
 
 
 EXPORTS = {"req_order": 0, "tiles": 1, "req_nslots": 2, "unit_req": 3, "req_blk_off": 4,
-           "req_blk": 5}
+           "req_blk": 5, "unit_boff": 6, "chunk_u0": 7, "chunk_u1": 8, "unit_nseg": 9,
+           "chunk_lo": 10}
 
 
 class Plan:

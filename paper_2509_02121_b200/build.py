@@ -26,13 +26,17 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, extra: list[str] | None = None) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, extra: list[str] | None = None,
+          lib: str = LIB, build_dir: str = BUILD) -> str:
+    """Compile the sources into `lib` (default: the in-tree libhalo_attn.so).  `extra` nvcc
+    flags + a different `lib`/`build_dir` give debug variants (e.g. -DHALO_K1_TRACE)."""
+    BUILD_ = build_dir
+    os.makedirs(BUILD_, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "halo_attn.h")]
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(BUILD_, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-c", s, "-o", o]
@@ -50,14 +54,20 @@ def build(verbose: bool = False, force: bool = False, extra: list[str] | None = 
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt",
+    if force or jobs or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt",
                "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib
+
+
+def build_trace() -> str:
+    """Debug variant with the K1 timeline trace (never used by tests or bench)."""
+    return build(extra=["-DHALO_K1_TRACE"], lib=os.path.join(PKG, "libhalo_attn_trace.so"),
+                 build_dir=os.path.join(PKG, "_build_trace"))
 
 
 if __name__ == "__main__":

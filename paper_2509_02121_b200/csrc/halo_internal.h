@@ -10,6 +10,9 @@ namespace halo {
 constexpr int kBlockTok = 16;       // tokens per KV block
 constexpr int kK1Rows = 128;        // K1 tile rows (UMMA M)
 constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
+constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N above this; bounded by smem)
+constexpr int kK2Warps = 12;        // K2 warps per CTA (one CTA per SM)
+constexpr int kK2Queues = 32;       // independent work queues for K2's dynamic tail chunks
 constexpr int kBlkCountShift = 27;  // K2 block entry: block | (ntok-1) << 27
 constexpr uint32_t kBlkMask = (1u << kBlkCountShift) - 1;
 
@@ -38,7 +41,25 @@ struct PlanDev {
     const int32_t *req_nslots;   // [nreq]
     float *part_o;               // [max_slots][nreq][Hq][D]
     float *part_lse;             // [max_slots][nreq][Hq]
-    int32_t ntiles, nreq, nunits, max_slots;
+    // K2 schedule: unit u = (request unit_req[u / hkv], kv head u % hkv) covers global block
+    // indices [unit_boff[u], unit_boff[u+1]).  The sequence is cut into chunks
+    // [chunk_lo[c], chunk_lo[c+1]): chunk w < nwarps is warp w's first (static) chunk, the
+    // rest are taken from an atomic queue (sched[0]); chunk c visits units
+    // [chunk_u0[c], chunk_u1[c]).  A unit cut by chunk boundaries writes nseg partial
+    // states (slots unit_seg..) merged by the last arriving piece.
+    const int32_t *unit_boff;    // [nunits + 1]
+    const int32_t *chunk_lo;     // [nchunks + 1]
+    const int32_t *unit_chunk0;  // [nunits] first chunk visiting the unit
+    const int32_t *chunk_u0;     // [nchunks]
+    const int32_t *chunk_u1;     // [nchunks]
+    const int32_t *unit_nseg;    // [nunits]
+    const int32_t *unit_seg;     // [nunits] first scratch slot (-1 if nseg == 1)
+    int32_t *unit_count;         // [nunits] arrival counters (zero between launches)
+    int32_t *sched;              // [2 + kK2Queues]: -, warps exited, per-queue next index
+                                 // (zero between launches)
+    float *seg_o;                // [nseg_total][g][D]  unnormalised o (base-2 state)
+    float *seg_ml;               // [nseg_total][g][2]  (m, l)
+    int32_t ntiles, nreq, nunits, max_slots, nwarps, nchunks, nblocks;
 };
 
 struct PoolGeom {
@@ -49,6 +70,7 @@ struct PoolGeom {
 // ---- launchers (kernels_*.cu) ----
 // K1: tcgen05/TMEM prefix attention -> normalised fp32 partials + lse (natural log).
 cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v,
+                               const CUtensorMap *tmap_k8, const CUtensorMap *tmap_v8,
                                const PlanDev &p, const PoolGeom &g, int layer,
                                const void *q, float scale, cudaStream_t s);
 // K2+K3: paged-suffix decode with the fused log-sum-exp merge of the K1 partials.

@@ -9,26 +9,50 @@
 // the design goal is HBM bandwidth.
 //
 // B200 design:
-//  * warp-persistent streaming: every warp owns a ring of kStages smem stages and walks
-//    work units (r, j) with a grid stride; its lane 0 issues one 1-D bulk async copy
-//    (cp.async.bulk, TMA engine) per 4-KiB K slab and V slab of a 16-token block, with
-//    completion on a per-stage mbarrier.  Prefetch runs ahead ACROSS unit boundaries, so
-//    short suffixes do not drain the pipe.  Each K/V element is read from HBM once for
-//    all g q-heads of its kv head (GQA reuse).
+//  * dynamic schedule: the blocks of all (request, kv head) units form one sequence cut
+//    into chunks of a few blocks; warps (148 SMs x kK2Warps) take chunks from an atomic
+//    queue, so SMs that stream faster take more work and the tail stays short whatever the
+//    suffix lengths.  A unit cut by chunk boundaries leaves one partial softmax state per
+//    piece; the last piece to finish (atomic arrival counter) merges them in a fixed
+//    order -> bit-deterministic results.
+//  * warp-level streaming: every warp owns a ring of kStages smem stages; its lane 0 issues
+//    one 1-D bulk async copy (cp.async.bulk, TMA engine) per 4-KiB K slab and V slab of a
+//    16-token block, completion on a per-stage mbarrier; prefetch runs across unit
+//    boundaries.  Each K/V element is read from HBM once for all g q-heads (GQA reuse).
 //  * compute from smem on CUDA cores: a token row is split over d/8 lanes (16-B LDS per
 //    lane); q.k partial sums of the g heads are combined with a transpose-reduce
 //    (log2(d/8)+g-1 shuffles instead of g*log2(d/8)), fp32x2 FMAs (FFMA2) for the dot
 //    products and the P.V update, online softmax in base 2 with fp32 state.
 //  * K3 epilogue: merge the suffix state with the normalised fp32 K1 partials of the
-//    request (slots in a fixed order -> bit-deterministic), write fp32 out and lse.
+//    request (slots in a fixed order), write fp32 out and lse.
 #include "halo_internal.h"
 #include "ptx.h"
+
+#include <cstdlib>
+
+#ifdef HALO_K1_TRACE
+// Debug: per-warp [start, first data, end] %globaltimer of the last launch.
+__device__ unsigned long long *g_k2_trace = nullptr;
+extern "C" int halo_debug_k2_trace(void *buf) {
+    return (int)cudaMemcpyToSymbol(g_k2_trace, &buf, sizeof(buf));
+}
+#define K2_TRACE(slot)                                                                  \
+    do {                                                                                \
+        if (lane == 0 && g_k2_trace) {                                                  \
+            unsigned long long t_;                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+            g_k2_trace[(blockIdx.x * kWarps + warp) * 4 + (slot)] = t_;                 \
+        }                                                                               \
+    } while (0)
+#else
+#define K2_TRACE(slot) do { } while (0)
+#endif
 
 namespace halo {
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kStages = 3;
+constexpr int kWarps = kK2Warps;
+constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -40,6 +64,7 @@ struct SuffixArgs {
     float *out, *lse;
     int32_t hkv, hq;
     float qscale;                     // scale * log2(e)
+    int32_t load_mode;                // 0: cp.async.bulk (TMA) per slab, 1: cp.async 16 B per lane
 };
 
 template <int D, int G>
@@ -51,7 +76,8 @@ struct Shape {
     static constexpr int STAGE = 2 * SLAB;          // K + V
     static constexpr int RING = kStages * STAGE;
     static constexpr int PS = kBlockTok * G * 4;    // p scratch
-    static constexpr int WARP_SMEM = RING + PS + 16 * 4 + kStages * 8;
+    static constexpr int CRING = 8;                 // acquired chunk ids (producer -> consumer)
+    static constexpr int WARP_SMEM = RING + PS + 16 * 4 + kStages * 8 + CRING * 4;
     static constexpr int WARP_SMEM_AL = (WARP_SMEM + 127) / 128 * 128;
     static_assert(G <= LPT, "transpose-reduce needs g <= d/8");
 };
@@ -60,7 +86,6 @@ struct Shape {
 // full sum of head c / (LPT/G) in v[0].
 template <int G, int LPT>
 __device__ __forceinline__ float transpose_reduce(float (&v)[G], int c) {
-    int n = G;
     int mask = LPT / 2;
 #pragma unroll
     for (int lvl = 0; (G >> lvl) > 1; ++lvl) {
@@ -72,12 +97,63 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[G], int c) {
             const float send = upper ? v[i] : v[i + half];
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
         }
-        n = half;
         mask >>= 1;
     }
 #pragma unroll
     for (int m = LPT / G / 2; m >= 1; m >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
     return v[0];
+}
+
+// Final merge of a unit's suffix state (base-2 max mh, sum lh, unnormalised o) with the
+// request's K1 partials, then the fp32 output / lse store.  Lanes of token group 0 only.
+template <int D, int G>
+__device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head, int c,
+                                         const float (&mh)[G], const float (&lh)[G],
+                                         float2 (&o2)[G][4]) {
+    const PlanDev &P = a.p;
+    const int nslots = P.req_nslots[req];
+    float M[G], L[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) M[h] = (lh[h] > 0.f) ? mh[h] + __log2f(lh[h]) : -INFINITY;
+    const int64_t slot_stride = (int64_t)P.nreq * a.hq;
+    for (int sl = 0; sl < nslots; ++sl) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            const float lp = P.part_lse[sl * slot_stride + (int64_t)req * a.hq + head * G + h] * kLog2e;
+            M[h] = fmaxf(M[h], lp);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        const float ws = (lh[h] > 0.f) ? ptx::ex2(mh[h] - M[h]) : 0.f;
+        L[h] = lh[h] * ws;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o2[h][i] = ptx::fmul2(o2[h][i], make_float2(ws, ws));
+    }
+    for (int sl = 0; sl < nslots; ++sl) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            const int64_t row = sl * slot_stride + (int64_t)req * a.hq + head * G + h;
+            const float w = ptx::ex2(P.part_lse[row] * kLog2e - M[h]);
+            L[h] += w;
+            const float4 *po = reinterpret_cast<const float4 *>(P.part_o + row * D + c * 8);
+            const float4 x0 = po[0], x1 = po[1];
+            const float2 ww = make_float2(w, w);
+            o2[h][0] = ptx::ffma2(ww, make_float2(x0.x, x0.y), o2[h][0]);
+            o2[h][1] = ptx::ffma2(ww, make_float2(x0.z, x0.w), o2[h][1]);
+            o2[h][2] = ptx::ffma2(ww, make_float2(x1.x, x1.y), o2[h][2]);
+            o2[h][3] = ptx::ffma2(ww, make_float2(x1.z, x1.w), o2[h][3]);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        const float inv = 1.f / L[h];
+        float4 *dst = reinterpret_cast<float4 *>(a.out + ((int64_t)req * a.hq + head * G + h) * D + c * 8);
+        dst[0] = make_float4(o2[h][0].x * inv, o2[h][0].y * inv, o2[h][1].x * inv, o2[h][1].y * inv);
+        dst[1] = make_float4(o2[h][2].x * inv, o2[h][2].y * inv, o2[h][3].x * inv, o2[h][3].y * inv);
+        if (a.lse != nullptr && c == h)
+            a.lse[(int64_t)req * a.hq + head * G + h] = (M[h] + __log2f(L[h])) * kLn2;
+    }
 }
 
 template <int D, int G>
@@ -89,9 +165,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     float *ps = reinterpret_cast<float *>(ws + S::RING);
     float *alph = ps + kBlockTok * G;
     uint64_t *full = reinterpret_cast<uint64_t *>(alph + 16);
+    int32_t *cring = reinterpret_cast<int32_t *>(full + kStages);
 
+    K2_TRACE(0);
     if (lane == 0) {
-        for (int s = 0; s < kStages; ++s) ptx::mbar_init(&full[s], 1);
+        for (int s = 0; s < kStages; ++s) ptx::mbar_init(&full[s], a.load_mode ? 32 : 1);
         ptx::fence_barrier_init();
     }
     __syncwarp();
@@ -102,53 +180,110 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     const int hsel = c / (S::LPT / G);
     const bool head_writer = (c % (S::LPT / G)) == 0;
     const int gw = blockIdx.x * kWarps + warp;
-    const int nw = gridDim.x * kWarps;
+    if (gw >= P.nwarps) return;
     const uint16_t *pk = a.pool_k + a.layer_off;
     const uint16_t *pv = a.pool_v + a.layer_off;
 
-    // ---- producer cursor (all lanes track it; lane 0 issues) ----
-    int p_unit = gw, p_blk = 0, p_beg = 0, p_end = 0, p_head = 0;
-    uint32_t p_count = 0, c_count = 0;
-    auto load_unit = [&](int u, int &beg, int &end, int &head, int &req) {
-        req = P.unit_req[u / a.hkv];
-        head = u % a.hkv;
-        beg = P.req_blk_off[req];
-        end = P.req_blk_off[req + 1];
+    // ---- producer: walks the blocks of the chunks it acquires (all lanes track it) ----
+    int pc = -1, phi = 0, px = 0, pu = 0, p_bu = 0, p_eu = 0, p_rb = 0, p_head = 0;
+    uint32_t p_count = 0, c_count = 0, p_chunks = 0, c_chunks = 0;
+    auto p_load_unit = [&]() {
+        p_bu = P.unit_boff[pu];
+        p_eu = P.unit_boff[pu + 1];
+        const int req = P.unit_req[pu / a.hkv];
+        p_head = pu % a.hkv;
+        p_rb = P.req_blk_off[req];
     };
-    if (p_unit < P.nunits) {
-        int req;
-        load_unit(p_unit, p_beg, p_end, p_head, req);
-    }
+    // The first chunk of warp w is chunk w (static: no atomic, neighbouring warps stream
+    // neighbouring slabs); later chunks come from the queue, fetched one acquisition ahead
+    // so the atomic's latency is hidden.
+    // Tail chunks [nwarps, nchunks) are spread over kK2Queues contiguous queues; warp w
+    // starts at queue w % kK2Queues and steals from the following queues when it runs dry.
+    const int ntail = max(P.nchunks - P.nwarps, 0);
+    const int per_q = (ntail + kK2Queues - 1) / kK2Queues;
+    int qcur = gw % kK2Queues, qtried = 0;
+    auto next_tail = [&]() -> int {
+        while (qtried < kK2Queues) {
+            const int base = qcur * per_q;
+            const int size = min(per_q, ntail - base);
+            if (size > 0) {
+                const int i = atomicAdd(&P.sched[2 + qcur], 1);
+                if (i < size) return P.nwarps + base + i;
+            }
+            qcur = (qcur + 1) % kK2Queues;
+            ++qtried;
+        }
+        return P.nchunks;
+    };
+    int next_c = gw;
+    auto acquire = [&]() {
+        int c = __shfl_sync(0xffffffffu, next_c, 0);
+        if (c >= P.nchunks) c = -1;
+        else if (lane == 0) next_c = next_tail();
+        if (lane == 0) cring[p_chunks % S::CRING] = c;
+        ++p_chunks;
+        pc = c;
+        if (c >= 0) {
+            px = P.chunk_lo[c];
+            phi = P.chunk_lo[c + 1];
+            pu = P.chunk_u0[c];
+            p_load_unit();
+        }
+    };
+    acquire();
     auto fill = [&]() {
-        while (p_unit < P.nunits && p_count - c_count < (uint32_t)kStages) {
-            if (p_beg + p_blk < p_end) {
+        while (pc >= 0 && p_count - c_count < (uint32_t)kStages) {
+            if (px >= phi) {
+                acquire();
+                continue;
+            }
+            while (px >= p_eu) {  // next unit (skips zero-length units)
+                ++pu;
+                p_load_unit();
+            }
+            const int st = p_count % kStages;
+            uint8_t *dst = ws + st * S::STAGE;
+            if (a.load_mode == 0) {
                 if (lane == 0) {
-                    const uint32_t e = P.req_blk[p_beg + p_blk];
-                    const int64_t blk = e & kBlkMask;
-                    const int64_t off = (blk * a.hkv + p_head) * (kBlockTok * D);
-                    const int st = p_count % kStages;
-                    uint8_t *dst = ws + st * S::STAGE;
+                    const uint32_t e = P.req_blk[p_rb + (px - p_bu)];
+                    const int64_t off = ((int64_t)(e & kBlkMask) * a.hkv + p_head) * (kBlockTok * D);
                     ptx::mbar_arrive_expect_tx(&full[st], S::STAGE);
                     ptx::bulk_g2s(dst, pk + off, S::SLAB, &full[st]);
                     ptx::bulk_g2s(dst + S::SLAB, pv + off, S::SLAB, &full[st]);
                 }
-                ++p_blk;
-                ++p_count;
             } else {
-                p_unit += nw;
-                p_blk = 0;
-                if (p_unit < P.nunits) {
-                    int req;
-                    load_unit(p_unit, p_beg, p_end, p_head, req);
+                const uint32_t e = P.req_blk[p_rb + (px - p_bu)];
+                const int64_t off = ((int64_t)(e & kBlkMask) * a.hkv + p_head) * (kBlockTok * D);
+                const uint8_t *gk = reinterpret_cast<const uint8_t *>(pk + off);
+                const uint8_t *gv = reinterpret_cast<const uint8_t *>(pv + off);
+#pragma unroll
+                for (int i = 0; i < S::SLAB / 16 / 32; ++i) {
+                    const int o = (i * 32 + lane) * 16;
+                    ptx::cp_async16(dst + o, gk + o);
+                    ptx::cp_async16(dst + S::SLAB + o, gv + o);
                 }
+                ptx::cp_async_mbar_arrive(&full[st]);
             }
+            ++px;
+            ++p_count;
         }
     };
     fill();
 
-    for (int u = gw; u < P.nunits; u += nw) {
-        int beg, end, head, req;
-        load_unit(u, beg, end, head, req);
+    for (;;) {
+        fill();  // makes sure the next chunk id has been acquired
+        __syncwarp();
+        const int cc = cring[c_chunks % S::CRING];
+        ++c_chunks;
+        if (cc < 0) break;
+        const int lo = P.chunk_lo[cc], hi = P.chunk_lo[cc + 1];
+        const int u_begin = P.chunk_u0[cc], u_end = P.chunk_u1[cc];
+    for (int u = u_begin; u < u_end; ++u) {
+        const int bu = P.unit_boff[u], eu = P.unit_boff[u + 1];
+        const int xs = max(bu, lo), xe = min(eu, hi);
+        const int req = P.unit_req[u / a.hkv];
+        const int head = u % a.hkv;
+        const int rb = P.req_blk_off[req] - bu;
         // q rows of the g heads of kv head `head`, this lane's 8 dims, pre-scaled.
         float2 q2[G][4];
 #pragma unroll
@@ -169,11 +304,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
 #pragma unroll
             for (int i = 0; i < 4; ++i) o2[h][i] = make_float2(0.f, 0.f);
 
-        for (int b = beg; b < end; ++b) {
+        for (int x = xs; x < xe; ++x) {
             fill();
             const int st = c_count % kStages;
-            const int ntok = (int)(P.req_blk[b] >> kBlkCountShift) + 1;
+            const int ntok = (int)(P.req_blk[rb + x] >> kBlkCountShift) + 1;
             ptx::mbar_wait(&full[st], (c_count / kStages) & 1);
+            if (c_count == 0) K2_TRACE(1);
             const uint16_t *ks = reinterpret_cast<const uint16_t *>(ws + st * S::STAGE);
             const uint16_t *vs = ks + kBlockTok * D;
 
@@ -187,9 +323,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 float part[G];
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
-                    float2 acc = make_float2(0.f, 0.f);
+                    float2 acc = ptx::fmul2(q2[h][0], ptx::bf2_to_f2(w[0]));
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc = ptx::ffma2(q2[h][i], ptx::bf2_to_f2(w[i]), acc);
+                    for (int i = 1; i < 4; ++i) acc = ptx::ffma2(q2[h][i], ptx::bf2_to_f2(w[i]), acc);
                     part[h] = acc.x + acc.y;
                 }
                 const float sc = transpose_reduce<G, S::LPT>(part, c);
@@ -268,54 +404,73 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             mh[h] = __shfl_sync(0xffffffffu, m, h * (S::LPT / G));
             lh[h] = __shfl_sync(0xffffffffu, l, h * (S::LPT / G));
         }
-        if (hw == 0) {
-        // ---- K3: log-sum-exp merge with the prefix partials (base 2) ----
-        const int nslots = P.req_nslots[req];
-        float M[G], L[G];
+        const int nseg = P.unit_nseg[u];
+        if (nseg == 1) {
+            if (hw == 0) finalize<D, G>(a, req, head, c, mh, lh, o2);
+        } else {
+            // ---- stream-K: publish this piece's state; the last piece merges them all ----
+            const int seg = cc - P.unit_chunk0[u];
+            const int slot = P.unit_seg[u] + seg;
+            if (hw == 0) {
 #pragma unroll
-        for (int h = 0; h < G; ++h) M[h] = (lh[h] > 0.f) ? mh[h] + __log2f(lh[h]) : -INFINITY;
-        const int64_t slot_stride = (int64_t)P.nreq * a.hq;
-        for (int sl = 0; sl < nslots; ++sl) {
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const float lp = P.part_lse[sl * slot_stride + (int64_t)req * a.hq + head * G + h] * kLog2e;
-                M[h] = fmaxf(M[h], lp);
+                for (int h = 0; h < G; ++h) {
+                    float4 *dst = reinterpret_cast<float4 *>(P.seg_o + ((int64_t)slot * G + h) * D + c * 8);
+                    dst[0] = make_float4(o2[h][0].x, o2[h][0].y, o2[h][1].x, o2[h][1].y);
+                    dst[1] = make_float4(o2[h][2].x, o2[h][2].y, o2[h][3].x, o2[h][3].y);
+                }
+                if (c < G) *reinterpret_cast<float2 *>(P.seg_ml + ((int64_t)slot * G + c) * 2) = make_float2(mh[c], lh[c]);
             }
-        }
+            __threadfence();
+            __syncwarp();
+            int old = 0;
+            if (lane == 0) old = atomicAdd(&P.unit_count[u], 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == nseg - 1) {
+                __threadfence();
+                if (lane == 0) P.unit_count[u] = 0;  // ready for the next launch
+                if (hw == 0) {
+                    // merge all pieces in segment order (deterministic), from L2
+                    float M[G], L[G];
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
-            const float ws_ = (lh[h] > 0.f) ? ptx::ex2(mh[h] - M[h]) : 0.f;
-            L[h] = lh[h] * ws_;
+                    for (int h = 0; h < G; ++h) { M[h] = -INFINITY; L[h] = 0.f; }
+                    const int base = P.unit_seg[u];
+                    for (int sg = 0; sg < nseg; ++sg)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) o2[h][i] = ptx::fmul2(o2[h][i], make_float2(ws_, ws_));
-        }
-        for (int sl = 0; sl < nslots; ++sl) {
+                        for (int h = 0; h < G; ++h)
+                            M[h] = fmaxf(M[h], __ldcg(P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
 #pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const int64_t row = sl * slot_stride + (int64_t)req * a.hq + head * G + h;
-                const float w = ptx::ex2(P.part_lse[row] * kLog2e - M[h]);
-                L[h] += w;
-                const float4 *po = reinterpret_cast<const float4 *>(P.part_o + row * D + c * 8);
-                const float4 x0 = po[0], x1 = po[1];
-                const float2 ww = make_float2(w, w);
-                o2[h][0] = ptx::ffma2(ww, make_float2(x0.x, x0.y), o2[h][0]);
-                o2[h][1] = ptx::ffma2(ww, make_float2(x0.z, x0.w), o2[h][1]);
-                o2[h][2] = ptx::ffma2(ww, make_float2(x1.x, x1.y), o2[h][2]);
-                o2[h][3] = ptx::ffma2(ww, make_float2(x1.z, x1.w), o2[h][3]);
+                    for (int h = 0; h < G; ++h)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) o2[h][i] = make_float2(0.f, 0.f);
+                    for (int sg = 0; sg < nseg; ++sg) {
+#pragma unroll
+                        for (int h = 0; h < G; ++h) {
+                            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(
+                                P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
+                            const float w = (ml.y > 0.f) ? ptx::ex2(ml.x - M[h]) : 0.f;
+                            L[h] += ml.y * w;
+                            const float4 *src = reinterpret_cast<const float4 *>(
+                                P.seg_o + ((int64_t)(base + sg) * G + h) * D + c * 8);
+                            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                            const float2 ww = make_float2(w, w);
+                            o2[h][0] = ptx::ffma2(ww, make_float2(x0.x, x0.y), o2[h][0]);
+                            o2[h][1] = ptx::ffma2(ww, make_float2(x0.z, x0.w), o2[h][1]);
+                            o2[h][2] = ptx::ffma2(ww, make_float2(x1.x, x1.y), o2[h][2]);
+                            o2[h][3] = ptx::ffma2(ww, make_float2(x1.z, x1.w), o2[h][3]);
+                        }
+                    }
+                    finalize<D, G>(a, req, head, c, M, L, o2);
+                }
             }
-        }
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-            const float inv = 1.f / L[h];
-            float4 *dst = reinterpret_cast<float4 *>(a.out + ((int64_t)req * a.hq + head * G + h) * D + c * 8);
-            dst[0] = make_float4(o2[h][0].x * inv, o2[h][0].y * inv, o2[h][1].x * inv, o2[h][1].y * inv);
-            dst[1] = make_float4(o2[h][2].x * inv, o2[h][2].y * inv, o2[h][3].x * inv, o2[h][3].y * inv);
-            if (a.lse != nullptr && c == h)
-                a.lse[(int64_t)req * a.hq + head * G + h] = (M[h] + __log2f(L[h])) * kLn2;
-        }
         }
         __syncwarp();
     }
+    }
+    if (lane == 0 && atomicAdd(&P.sched[1], 1) == P.nwarps - 1) {  // last warp out: reset queues
+        P.sched[1] = 0;
+        for (int q = 0; q < kK2Queues; ++q) P.sched[2 + q] = 0;
+    }
+    K2_TRACE(2);
 }
 
 template <int D, int G>
@@ -331,10 +486,8 @@ cudaError_t launch_t(const SuffixArgs &a, int num_sms, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    const int units_per_cta = kWarps;
-    int grid = (a.p.nunits + units_per_cta - 1) / units_per_cta;
-    if (grid > num_sms) grid = num_sms;  // 1 CTA (8 persistent warps) per SM
-    if (grid < 1) return cudaSuccess;
+    if (a.p.nunits == 0) return cudaSuccess;
+    const int grid = (a.p.nwarps + kWarps - 1) / kWarps;  // = num_sms: one CTA per SM
     kern<<<grid, kWarps * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -355,6 +508,11 @@ cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void
     a.hkv = g.hkv;
     a.hq = g.hq;
     a.qscale = scale * kLog2e;
+    static const int load_mode = [] {
+        const char *e = getenv("HALO_K2_LOAD");
+        return e ? atoi(e) : 0;
+    }();
+    a.load_mode = load_mode;
     const int G = g.hq / g.hkv;
 #define HALO_K2_CASE(DD, GG) \
     if (g.d == DD && G == GG) return launch_t<DD, GG>(a, num_sms, s);

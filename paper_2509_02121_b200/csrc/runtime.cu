@@ -252,7 +252,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-halo_status make_tmap(halo_pool p, void *base, CUtensorMap *out) {
+halo_status make_tmap(halo_pool p, void *base, CUtensorMap *out, int box_blocks) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -268,7 +268,7 @@ halo_status make_tmap(halo_pool p, void *base, CUtensorMap *out) {
                           (cuuint64_t)c.num_layers * (cuuint64_t)c.capacity_blocks};
     cuuint64_t strides[3] = {(cuuint64_t)c.head_dim * 2, (cuuint64_t)kBlockTok * c.head_dim * 2,
                              (cuuint64_t)c.num_kv_heads * kBlockTok * c.head_dim * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)kBlockTok, 1, 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)kBlockTok, 1, (cuuint32_t)box_blocks};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -300,7 +300,7 @@ int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_
         if (n.tensor) max_tok = std::max<int64_t>(max_tok, n.node->ntok);
     if (max_tok == 0) return kK1Tok;
     const int64_t kOvh = 256;
-    const int64_t nk = ceil_div(max_tok, kK1Tok);
+    const int64_t nk = ceil_div(std::min<int64_t>(max_tok, kK1MaxTileTok), kK1Tok);
     const int64_t step = std::max<int64_t>(1, nk / 256);
     double best = 1e300;
     int best_c = (int)(nk * kK1Tok);
@@ -311,7 +311,7 @@ int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_
         for (auto &n : ns) {
             if (!n.tensor) continue;
             const int64_t tok = n.node->ntok;
-            int64_t s = std::min<int64_t>(ceil_div(tok, C), max_splits);
+            int64_t s = std::max(std::min<int64_t>(ceil_div(tok, C), max_splits), ceil_div(tok, kK1MaxTileTok));
             const int64_t ch = ceil_div(ceil_div(tok, s), kK1Tok) * kK1Tok;
             s = ceil_div(tok, ch);
             const int64_t base = ceil_div((int64_t)(n.r1 - n.r0) * g, kK1Rows) * hkv;
@@ -432,7 +432,8 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
         for (auto &n : ns) {
             if (!n.tensor) continue;
             const int64_t tok = n.node->ntok;
-            const int64_t s = std::min<int64_t>(pl->opt.force_splits, ceil_div(tok, kK1Tok));
+            const int64_t s = std::max(std::min<int64_t>(pl->opt.force_splits, ceil_div(tok, kK1Tok)),
+                                       ceil_div(tok, kK1MaxTileTok));
             n.chunk = (int)(ceil_div(ceil_div(tok, s), kK1Tok) * kK1Tok);
             n.splits = (int)ceil_div(tok, n.chunk);
         }
@@ -441,7 +442,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
         for (auto &n : ns) {
             if (!n.tensor) continue;
             const int64_t tok = n.node->ntok;
-            const int64_t s = std::min<int64_t>(ceil_div(tok, C), max_splits);
+            const int64_t s = std::max(std::min<int64_t>(ceil_div(tok, C), max_splits), ceil_div(tok, kK1MaxTileTok));
             n.chunk = (int)(ceil_div(ceil_div(tok, s), kK1Tok) * kK1Tok);
             n.splits = (int)ceil_div(tok, n.chunk);
         }
@@ -529,6 +530,59 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
     std::stable_sort(pl->unit_req.begin(), pl->unit_req.end(), [&](int a, int b) {
         return pl->req_blk_off[a + 1] - pl->req_blk_off[a] > pl->req_blk_off[b + 1] - pl->req_blk_off[b];
     });
+    // 12b. K2 schedule: a static first round (one chunk per warp) then small dynamic chunks
+    {
+        const int U = nreq * hkv;
+        const int64_t W = (int64_t)p->num_sms * kK2Warps;
+        pl->unit_boff.assign(U + 1, 0);
+        for (int u = 0; u < U; ++u) {
+            const int req = pl->unit_req[u / hkv];
+            pl->unit_boff[u + 1] = pl->unit_boff[u] + (pl->req_blk_off[req + 1] - pl->req_blk_off[req]);
+        }
+        const int64_t Btot = pl->unit_boff[U];
+        std::vector<int32_t> &lo = pl->chunk_lo;
+        lo.assign(1, 0);
+        if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
+            for (int64_t x = pl->opt.k2_chunk_blocks; x < Btot; x += pl->opt.k2_chunk_blocks) lo.push_back((int32_t)x);
+        } else {
+            // static equal-bytes partition: warp w gets [w*Btot/W, (w+1)*Btot/W).  Measured
+            // alternatives (snapping cuts to unit ends: uneven chunks; a dynamic tail of small
+            // chunks: per-chunk setup latencies) were slower on B200.
+            for (int64_t w = 1; w < W; ++w) {
+                const int64_t b = w * Btot / W;
+                if (b > lo.back() && b < Btot) lo.push_back((int32_t)b);
+            }
+        }
+        lo.push_back((int32_t)Btot);
+        if (lo.size() < 2) lo.push_back(0);
+        const int64_t nchunks = (int64_t)lo.size() - 1;
+        auto chunk_of = [&](int64_t xx) {  // chunk containing block index xx (Btot -> last)
+            if (xx >= Btot) return nchunks - 1;
+            return (int64_t)(std::upper_bound(lo.begin(), lo.end(), (int32_t)xx) - lo.begin()) - 1;
+        };
+        pl->chunk_u0.assign(nchunks, U);
+        pl->chunk_u1.assign(nchunks, 0);
+        pl->unit_nseg.resize(U);
+        pl->unit_seg.resize(U);
+        pl->unit_chunk0.resize(U);
+        int32_t nseg_total = 0;
+        for (int uu = 0; uu < U; ++uu) {
+            const int64_t b = pl->unit_boff[uu], e = pl->unit_boff[uu + 1];
+            const int64_t c0 = chunk_of(b), c1 = e > b ? chunk_of(e - 1) : c0;
+            for (int64_t cc = c0; cc <= c1; ++cc) {
+                pl->chunk_u0[cc] = std::min(pl->chunk_u0[cc], uu);
+                pl->chunk_u1[cc] = std::max(pl->chunk_u1[cc], uu + 1);
+            }
+            const int nseg = (int)(c1 - c0 + 1);
+            pl->unit_chunk0[uu] = (int32_t)c0;
+            pl->unit_nseg[uu] = nseg;
+            pl->unit_seg[uu] = nseg > 1 ? nseg_total : -1;
+            if (nseg > 1) nseg_total += nseg;
+        }
+        for (int64_t cc = 0; cc < nchunks; ++cc)
+            if (pl->chunk_u0[cc] >= pl->chunk_u1[cc]) pl->chunk_u0[cc] = pl->chunk_u1[cc] = 0;
+        pl->nseg_total = nseg_total;
+    }
     // 13. info
     halo_plan_info &inf = pl->info;
     inf = halo_plan_info{};
@@ -562,6 +616,14 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const size_t o_boff = off; off = align16(off + (nreq + 1) * 4);
     const size_t o_blk = off; off = align16(off + pl->req_blk.size() * 4);
     const size_t o_nsl = off; off = align16(off + nreq * 4);
+    const int U = (int)pl->unit_nseg.size(), NC = (int)pl->chunk_u0.size();
+    const size_t o_uboff = off; off = align16(off + (U + 1) * 4);
+    const size_t o_clo = off; off = align16(off + (NC + 1) * 4);
+    const size_t o_uc0 = off; off = align16(off + U * 4);
+    const size_t o_cu0 = off; off = align16(off + NC * 4);
+    const size_t o_cu1 = off; off = align16(off + NC * 4);
+    const size_t o_unseg = off; off = align16(off + U * 4);
+    const size_t o_useg = off; off = align16(off + U * 4);
     const size_t total = off;
     pl->host_buf.resize(total);
     uint8_t *h = pl->host_buf.data();
@@ -573,6 +635,13 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     put(o_boff, pl->req_blk_off.data(), (nreq + 1) * 4);
     put(o_blk, pl->req_blk.data(), pl->req_blk.size() * 4);
     put(o_nsl, pl->req_nslots.data(), nreq * 4);
+    put(o_uboff, pl->unit_boff.data(), (U + 1) * 4);
+    put(o_clo, pl->chunk_lo.data(), (NC + 1) * 4);
+    put(o_uc0, pl->unit_chunk0.data(), U * 4);
+    put(o_cu0, pl->chunk_u0.data(), NC * 4);
+    put(o_cu1, pl->chunk_u1.data(), NC * 4);
+    put(o_unseg, pl->unit_nseg.data(), U * 4);
+    put(o_useg, pl->unit_seg.data(), U * 4);
     if (p->host_only) return HALO_OK;
 
     if (pl->dbuf_cap < total) {
@@ -596,6 +665,29 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
         HALO_CUDA(cudaMalloc(&pl->part, cap * 4));
         pl->part_cap = cap;
     }
+    const size_t seg_elems = (size_t)pl->nseg_total * (p->cfg.num_q_heads / p->cfg.num_kv_heads) *
+                             (p->cfg.head_dim + 2);
+    if (pl->seg_cap < seg_elems) {
+        if (pl->segbuf) {
+            HALO_CUDA(cudaStreamSynchronize(s));
+            cudaFree(pl->segbuf);
+            pl->segbuf = nullptr;
+        }
+        const size_t cap = seg_elems + seg_elems / 4 + 1024;
+        HALO_CUDA(cudaMalloc(&pl->segbuf, cap * 4));
+        pl->seg_cap = cap;
+    }
+    if (pl->counter_cap < (size_t)U + 2 + kK2Queues) {
+        if (pl->counters) {
+            HALO_CUDA(cudaStreamSynchronize(s));
+            cudaFree(pl->counters);
+            pl->counters = nullptr;
+        }
+        const size_t cap = U + U / 4 + 64 + kK2Queues;
+        HALO_CUDA(cudaMalloc(&pl->counters, cap * 4));
+        pl->counter_cap = cap;
+    }
+    HALO_CUDA(cudaMemsetAsync(pl->counters, 0, ((size_t)U + 2 + kK2Queues) * 4, s));
     HALO_CUDA(cudaMemcpyAsync(pl->dbuf, h, total, cudaMemcpyHostToDevice, s));
     uint8_t *d = static_cast<uint8_t *>(pl->dbuf);
     PlanDev &dv = pl->dev;
@@ -608,6 +700,21 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     dv.req_nslots = reinterpret_cast<const int32_t *>(d + o_nsl);
     dv.part_o = pl->part;
     dv.part_lse = pl->part + (size_t)pl->info.max_slots * nreq * p->cfg.num_q_heads * p->cfg.head_dim;
+    dv.unit_boff = reinterpret_cast<const int32_t *>(d + o_uboff);
+    dv.chunk_lo = reinterpret_cast<const int32_t *>(d + o_clo);
+    dv.unit_chunk0 = reinterpret_cast<const int32_t *>(d + o_uc0);
+    dv.chunk_u0 = reinterpret_cast<const int32_t *>(d + o_cu0);
+    dv.chunk_u1 = reinterpret_cast<const int32_t *>(d + o_cu1);
+    dv.unit_nseg = reinterpret_cast<const int32_t *>(d + o_unseg);
+    dv.unit_seg = reinterpret_cast<const int32_t *>(d + o_useg);
+    dv.unit_count = pl->counters;
+    dv.sched = pl->counters + U;
+    dv.nchunks = NC;
+    dv.nblocks = pl->unit_boff.empty() ? 0 : pl->unit_boff.back();
+    const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
+    dv.seg_o = pl->segbuf;
+    dv.seg_ml = pl->segbuf + (size_t)pl->nseg_total * gq * p->cfg.head_dim;
+    dv.nwarps = p->num_sms * kK2Warps;
     dv.ntiles = (int32_t)pl->tiles.size();
     dv.nreq = nreq;
     dv.nunits = nreq * p->cfg.num_kv_heads;
@@ -620,7 +727,7 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
     halo_pool p = pl->pool;
     cudaError_t e;
     if (mask & 1) {
-        e = launch_prefix_attn(&p->tmap_k, &p->tmap_v, pl->dev, p->geom, layer, q, scale, s);
+        e = launch_prefix_attn(&p->tmap_k, &p->tmap_v, &p->tmap_k8, &p->tmap_v8, pl->dev, p->geom, layer, q, scale, s);
         if (e != cudaSuccess) return fail(HALO_ECUDA, "prefix kernel launch: %s", cudaGetErrorString(e));
     }
     if (mask & 2) {
@@ -714,8 +821,10 @@ halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
         halo_status st = HALO_OK;
         if (cudaMemset(p->k, 0, bytes) != cudaSuccess || cudaMemset(p->v, 0, bytes) != cudaSuccess)
             st = fail(HALO_ECUDA, "cudaMemset of the pool failed");
-        if (st == HALO_OK) st = make_tmap(p, p->k, &p->tmap_k);
-        if (st == HALO_OK) st = make_tmap(p, p->v, &p->tmap_v);
+        if (st == HALO_OK) st = make_tmap(p, p->k, &p->tmap_k, 1);
+        if (st == HALO_OK) st = make_tmap(p, p->v, &p->tmap_v, 1);
+        if (st == HALO_OK) st = make_tmap(p, p->k, &p->tmap_k8, 8);
+        if (st == HALO_OK) st = make_tmap(p, p->v, &p->tmap_v8, 8);
         if (st != HALO_OK) {
             if (p->own_storage) {
                 cudaFree(p->k);
@@ -1031,6 +1140,8 @@ halo_status halo_decode_plan(halo_pool p, int32_t nreq, const int64_t *reqs, con
         if (fresh) {
             if (pl->dbuf) cudaFree(pl->dbuf);
             if (pl->part) cudaFree(pl->part);
+            if (pl->segbuf) cudaFree(pl->segbuf);
+            if (pl->counters) cudaFree(pl->counters);
             delete pl;
         }
         return st;
@@ -1143,6 +1254,11 @@ halo_status halo_plan_export(halo_plan pl, int32_t which, void *dst, int64_t cap
         case 3: src = pl->unit_req.data(); cnt = (int64_t)pl->unit_req.size(); break;
         case 4: src = pl->req_blk_off.data(); cnt = (int64_t)pl->req_blk_off.size(); break;
         case 5: src = pl->req_blk.data(); cnt = (int64_t)pl->req_blk.size(); break;
+        case 6: src = pl->unit_boff.data(); cnt = (int64_t)pl->unit_boff.size(); break;
+        case 7: src = pl->chunk_u0.data(); cnt = (int64_t)pl->chunk_u0.size(); break;
+        case 8: src = pl->chunk_u1.data(); cnt = (int64_t)pl->chunk_u1.size(); break;
+        case 9: src = pl->unit_nseg.data(); cnt = (int64_t)pl->unit_nseg.size(); break;
+        case 10: src = pl->chunk_lo.data(); cnt = (int64_t)pl->chunk_lo.size(); break;
         default: return fail(HALO_EINVAL, "unknown export %d", which);
     }
     *n = cnt;
@@ -1158,6 +1274,8 @@ halo_status halo_plan_destroy(halo_plan pl) {
         DeviceGuard dg(p);
         if (pl->dbuf) cudaFree(pl->dbuf);
         if (pl->part) cudaFree(pl->part);
+        if (pl->segbuf) cudaFree(pl->segbuf);
+        if (pl->counters) cudaFree(pl->counters);
         if (pl->q_stage) cudaFree(pl->q_stage);
         if (pl->o_stage) cudaFree(pl->o_stage);
         if (pl->l_stage) cudaFree(pl->l_stage);

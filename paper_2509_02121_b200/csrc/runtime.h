@@ -58,7 +58,8 @@ struct halo_pool_s {
     std::unordered_map<int64_t, halo::Request> requests;
     int64_t next_id = 1;
     int32_t plans_alive = 0;
-    CUtensorMap tmap_k{}, tmap_v{};
+    CUtensorMap tmap_k{}, tmap_v{};      // box: one 16-token block x 64 d
+    CUtensorMap tmap_k8{}, tmap_v8{};    // box: 8 consecutive blocks (128 tokens) x 64 d
     // migration
     ncclComm_t comm = nullptr;
     int32_t nranks = 0, rank = -1;
@@ -73,6 +74,8 @@ struct halo_plan_s {
     int32_t nreq = 0;
     halo_plan_options opt{};
     std::vector<int32_t> req_order, node_blocks, unit_req, req_blk_off, req_nslots;
+    std::vector<int32_t> unit_boff, chunk_lo, chunk_u0, chunk_u1, unit_chunk0, unit_nseg, unit_seg;
+    int32_t nseg_total = 0;
     std::vector<uint32_t> req_blk;
     std::vector<halo::PrefixTile> tiles;
     halo_plan_info info{};
@@ -81,6 +84,10 @@ struct halo_plan_s {
     size_t dbuf_cap = 0;
     float *part = nullptr;
     size_t part_cap = 0;
+    float *segbuf = nullptr;   // stream-K scratch (seg_o | seg_ml)
+    size_t seg_cap = 0;
+    int32_t *counters = nullptr;
+    size_t counter_cap = 0;
     halo::PlanDev dev{};
     // staging for halo_decode_layers with host buffers
     void *q_stage = nullptr;

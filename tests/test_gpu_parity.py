@@ -67,8 +67,8 @@ def check(wl, opt=None, layers=None, sample=None):
     return info, worst_o, worst_l
 
 
-def opts(min_rows=0, splits=0, max_splits=0):
-    return PlanOptions(min_rows, splits, max_splits, 0)
+def opts(min_rows=0, splits=0, max_splits=0, chunk=0):
+    return PlanOptions(min_rows, splits, max_splits, chunk)
 
 
 def test_toy_c0_folded():
@@ -85,6 +85,15 @@ def test_toy_c0_tensor_path_d64_g1():
 def test_ragged_tree(min_rows, splits):
     """depth-3 tree, partial blocks, no-prefix requests, 0-token initial suffixes, g=4."""
     check(make_config("ragged"), opts(min_rows, splits))
+
+
+@pytest.mark.parametrize("chunk", [1, 3, 16])
+def test_k2_work_queue_chunking(chunk):
+    """Units cut into many pieces by the K2 work queue merge back exactly (ragged suffixes,
+    zero-length-suffix requests, folded nodes)."""
+    check(make_config("ragged_suffix", layers=1, nreq=24, prefix=300, lo=1, hi=200),
+          opts(chunk=chunk))
+    check(make_config("ragged"), opts(min_rows=16, chunk=chunk))
 
 
 def test_fanout_small_k1_multi_mtile():

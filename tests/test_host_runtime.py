@@ -117,7 +117,8 @@ def plan_of(wl, **opt):
     reqs = ld.req_ids
     # one decode step appends a token to each request
     p.append(reqs, [1] * len(reqs))
-    o = PlanOptions(opt.get("min_rows", 0), opt.get("force_splits", 0), opt.get("max_splits", 0), 0)
+    o = PlanOptions(opt.get("min_rows", 0), opt.get("force_splits", 0), opt.get("max_splits", 0),
+                    opt.get("chunk", 0))
     return p, ld, p.plan(reqs, o)
 
 
@@ -205,3 +206,39 @@ def test_plan_rebuild_in_place():
     pl2 = p.plan(ld.req_ids[:5], reuse=pl)
     assert pl2 is pl and pl.info()["nreq"] == 5
     pl.destroy()
+
+
+@pytest.mark.parametrize("cfg,kw,cb", [("ragged", {}, 0), ("ragged", {}, 3),
+                                       ("ragged_suffix", {"layers": 1, "nreq": 40}, 0),
+                                       ("fanout", {"layers": 1, "nreq": 256, "suffix": 255}, 0),
+                                       ("toy", {}, 0), ("toy", {}, 16)])
+def test_k2_chunk_schedule_covers_every_block_once(cfg, kw, cb):
+    """K2's work queue: chunks of CB blocks tile [0, Btot); each unit is visited by exactly
+    the chunks it intersects (its nseg pieces), zero-length units by exactly one chunk."""
+    wl = make_config(cfg, **kw)
+    p, ld, pl = plan_of(wl, min_rows=64, chunk=cb)
+    boff = pl.export("unit_boff")
+    u0, u1 = pl.export("chunk_u0"), pl.export("chunk_u1")
+    nseg = pl.export("unit_nseg")
+    clo = pl.export("chunk_lo")
+    U, NC, Btot = len(boff) - 1, len(u0), int(boff[-1])
+    assert len(clo) == NC + 1 and clo[0] == 0 and clo[-1] == Btot
+    assert all(clo[i] < clo[i + 1] for i in range(NC)) or Btot == 0
+    if cb:
+        assert all(clo[i + 1] - clo[i] <= cb for i in range(NC))
+    visits = [[] for _ in range(U)]
+    covered = np.zeros(Btot, dtype=np.int32)
+    for c in range(NC):
+        lo, hi = clo[c], clo[c + 1]
+        for u in range(u0[c], u1[c]):
+            xs, xe = max(boff[u], lo), min(boff[u + 1], hi)
+            if boff[u + 1] > boff[u]:
+                assert xe > xs, (c, u)  # a chunk only lists units it intersects
+            visits[u].append(c)
+            covered[xs:xe] += 1
+    assert np.all(covered == 1)
+    for u in range(U):
+        assert len(visits[u]) == nseg[u] >= 1, (u, visits[u], nseg[u])
+        assert visits[u] == list(range(visits[u][0], visits[u][0] + nseg[u]))
+    pl.destroy()
+    p.destroy()

@@ -82,7 +82,8 @@ typedef struct {
                                 reads kv head floor(h/g) (reading R3)          */
     int32_t head_dim;        /* 64 or 128 */
     int32_t block_tokens;    /* must be HALO_BLOCK_TOKENS (16) */
-    int64_t capacity_blocks; /* blocks per layer */
+    int64_t capacity_blocks; /* blocks per layer; capacity_blocks * num_kv_heads <= 2^27
+                                and num_layers * capacity_blocks < 2^31 (EINVAL)      */
     void *k_storage;         /* optional caller-owned device memory for K (and V), each of
                                 >= halo_pool_storage_bytes(cfg) bytes, 256-B aligned;
                                 NULL => the library allocates (and frees) it.           */

@@ -11,9 +11,15 @@ constexpr int kBlockTok = 16;       // tokens per KV block
 constexpr int kK1Rows = 128;        // K1 tile rows (UMMA M)
 constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
 constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N above this; bounded by smem)
-constexpr int kK2Warps = 12;        // K2 warps per CTA (one CTA per SM)
-constexpr int kK2Queues = 32;       // independent work queues for K2's dynamic tail chunks
-constexpr int kBlkCountShift = 27;  // K2 block entry: block | (ntok-1) << 27
+#ifndef HALO_K2_WARPS
+#define HALO_K2_WARPS 8
+#endif
+#ifndef HALO_K2_STAGES
+#define HALO_K2_STAGES 2
+#endif
+constexpr int kK2Warps = HALO_K2_WARPS;    // K2 warps per CTA (one CTA per SM)
+constexpr int kK2Stages = HALO_K2_STAGES;  // K2 smem ring stages per warp (16-token K+V blocks)
+constexpr int kBlkCountShift = 27;  // K2 block entry: block | (ntok-1) << 27 (| unit start << 31)
 constexpr uint32_t kBlkMask = (1u << kBlkCountShift) - 1;
 
 // One K1 work tile: rows [row0, row0+nrows) of node n's (request x q-head-in-group) row
@@ -43,10 +49,15 @@ struct PlanDev {
     float *part_lse;             // [max_slots][nreq][Hq]
     // K2 schedule: unit u = (request unit_req[u / hkv], kv head u % hkv) covers global block
     // indices [unit_boff[u], unit_boff[u+1]).  The sequence is cut into chunks
-    // [chunk_lo[c], chunk_lo[c+1]): chunk w < nwarps is warp w's first (static) chunk, the
-    // rest are taken from an atomic queue (sched[0]); chunk c visits units
-    // [chunk_u0[c], chunk_u1[c]).  A unit cut by chunk boundaries writes nseg partial
-    // states (slots unit_seg..) merged by the last arriving piece.
+    // [chunk_lo[c], chunk_lo[c+1]); warp w processes chunks w, w + nwarps, ... (static);
+    // chunk c visits units [chunk_u0[c], chunk_u1[c]).  A unit cut by chunk boundaries
+    // writes nseg partial states (slots unit_seg..) merged by the last arriving piece.
+    // k2_ent[x] describes global block x: {slab | (ntok-1) << 27 | unit start << 31,
+    // q group row}, slab = pool block * hkv + kv head, q group row = request * hkv + head.
+    // unit_meta[2u], [2u+1] = {boff_begin, boff_end, request, kv head},
+    //                         {nslots, nseg, first seg slot, first chunk}.
+    const uint2 *k2_ent;         // [nblocks]
+    const int4 *unit_meta;       // [2 * nunits]
     const int32_t *unit_boff;    // [nunits + 1]
     const int32_t *chunk_lo;     // [nchunks + 1]
     const int32_t *unit_chunk0;  // [nunits] first chunk visiting the unit
@@ -55,8 +66,6 @@ struct PlanDev {
     const int32_t *unit_nseg;    // [nunits]
     const int32_t *unit_seg;     // [nunits] first scratch slot (-1 if nseg == 1)
     int32_t *unit_count;         // [nunits] arrival counters (zero between launches)
-    int32_t *sched;              // [2 + kK2Queues]: -, warps exited, per-queue next index
-                                 // (zero between launches)
     float *seg_o;                // [nseg_total][g][D]  unnormalised o (base-2 state)
     float *seg_ml;               // [nseg_total][g][2]  (m, l)
     int32_t ntiles, nreq, nunits, max_slots, nwarps, nchunks, nblocks;

@@ -206,6 +206,18 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Mixed-precision FMA (sm_100+, SASS FHFMA.BF16): acc + lo(a)*lo(b) / acc + hi(a)*hi(b),
+// a and b bf16 pairs; the product is exact in fp32, one rounding on the add.
+__device__ __forceinline__ float fma_bf16_lo(uint32_t a, uint32_t b, float acc) {
+    asm("{\n\t.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, al, bl, %0;\n\t}" : "+f"(acc) : "r"(a), "r"(b));
+    return acc;
+}
+__device__ __forceinline__ float fma_bf16_hi(uint32_t a, uint32_t b, float acc) {
+    asm("{\n\t.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, ah, bh, %0;\n\t}" : "+f"(acc) : "r"(a), "r"(b));
+    return acc;
+}
 // bf16 pair (one 32-bit word) -> two floats, exact.
 __device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));

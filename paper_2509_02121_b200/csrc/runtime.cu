@@ -530,7 +530,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
     std::stable_sort(pl->unit_req.begin(), pl->unit_req.end(), [&](int a, int b) {
         return pl->req_blk_off[a + 1] - pl->req_blk_off[a] > pl->req_blk_off[b + 1] - pl->req_blk_off[b];
     });
-    // 12b. K2 schedule: a static first round (one chunk per warp) then small dynamic chunks
+    // 12b. K2 schedule: static chunks, warp w takes chunks w, w + W, ...
     {
         const int U = nreq * hkv;
         const int64_t W = (int64_t)p->num_sms * kK2Warps;
@@ -582,6 +582,24 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
         for (int64_t cc = 0; cc < nchunks; ++cc)
             if (pl->chunk_u0[cc] >= pl->chunk_u1[cc]) pl->chunk_u0[cc] = pl->chunk_u1[cc] = 0;
         pl->nseg_total = nseg_total;
+        // per-block descriptors and per-unit metadata read by the kernel
+        pl->k2_ent.resize((size_t)Btot * 2);
+        pl->unit_meta.resize((size_t)U * 8);
+        for (int uu = 0; uu < U; ++uu) {
+            const int req = pl->unit_req[uu / hkv], head = uu % hkv;
+            const int32_t b0 = pl->unit_boff[uu], b1 = pl->unit_boff[uu + 1];
+            const int32_t rb = pl->req_blk_off[req];
+            for (int32_t x = b0; x < b1; ++x) {
+                const uint32_t e = pl->req_blk[rb + (x - b0)];
+                const uint32_t slab = (e & kBlkMask) * (uint32_t)hkv + (uint32_t)head;
+                pl->k2_ent[2 * (size_t)x] = slab | (e & ~kBlkMask) | (x == b0 ? 0x80000000u : 0u);
+                pl->k2_ent[2 * (size_t)x + 1] = (uint32_t)(req * hkv + head);
+            }
+            int32_t *um = &pl->unit_meta[(size_t)uu * 8];
+            um[0] = b0; um[1] = b1; um[2] = req; um[3] = head;
+            um[4] = pl->req_nslots[req]; um[5] = pl->unit_nseg[uu]; um[6] = pl->unit_seg[uu];
+            um[7] = pl->unit_chunk0[uu];
+        }
     }
     // 13. info
     halo_plan_info &inf = pl->info;
@@ -624,6 +642,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const size_t o_cu1 = off; off = align16(off + NC * 4);
     const size_t o_unseg = off; off = align16(off + U * 4);
     const size_t o_useg = off; off = align16(off + U * 4);
+    const size_t o_ent = off; off = align16(off + pl->k2_ent.size() * 4);
+    const size_t o_umeta = off; off = align16(off + pl->unit_meta.size() * 4);
     const size_t total = off;
     pl->host_buf.resize(total);
     uint8_t *h = pl->host_buf.data();
@@ -642,6 +662,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     put(o_cu1, pl->chunk_u1.data(), NC * 4);
     put(o_unseg, pl->unit_nseg.data(), U * 4);
     put(o_useg, pl->unit_seg.data(), U * 4);
+    put(o_ent, pl->k2_ent.data(), pl->k2_ent.size() * 4);
+    put(o_umeta, pl->unit_meta.data(), pl->unit_meta.size() * 4);
     if (p->host_only) return HALO_OK;
 
     if (pl->dbuf_cap < total) {
@@ -677,17 +699,17 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
         HALO_CUDA(cudaMalloc(&pl->segbuf, cap * 4));
         pl->seg_cap = cap;
     }
-    if (pl->counter_cap < (size_t)U + 2 + kK2Queues) {
+    if (pl->counter_cap < (size_t)U + 2) {
         if (pl->counters) {
             HALO_CUDA(cudaStreamSynchronize(s));
             cudaFree(pl->counters);
             pl->counters = nullptr;
         }
-        const size_t cap = U + U / 4 + 64 + kK2Queues;
+        const size_t cap = U + U / 4 + 64;
         HALO_CUDA(cudaMalloc(&pl->counters, cap * 4));
         pl->counter_cap = cap;
     }
-    HALO_CUDA(cudaMemsetAsync(pl->counters, 0, ((size_t)U + 2 + kK2Queues) * 4, s));
+    HALO_CUDA(cudaMemsetAsync(pl->counters, 0, ((size_t)U + 2) * 4, s));
     HALO_CUDA(cudaMemcpyAsync(pl->dbuf, h, total, cudaMemcpyHostToDevice, s));
     uint8_t *d = static_cast<uint8_t *>(pl->dbuf);
     PlanDev &dv = pl->dev;
@@ -708,7 +730,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     dv.unit_nseg = reinterpret_cast<const int32_t *>(d + o_unseg);
     dv.unit_seg = reinterpret_cast<const int32_t *>(d + o_useg);
     dv.unit_count = pl->counters;
-    dv.sched = pl->counters + U;
+    dv.k2_ent = reinterpret_cast<const uint2 *>(d + o_ent);
+    dv.unit_meta = reinterpret_cast<const int4 *>(d + o_umeta);
     dv.nchunks = NC;
     dv.nblocks = pl->unit_boff.empty() ? 0 : pl->unit_boff.back();
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
@@ -785,7 +808,7 @@ halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
     if (g != 1 && g != 2 && g != 4 && g != 8) return fail(HALO_EINVAL, "q heads per kv head must be 1, 2, 4 or 8");
     if (c.head_dim != 64 && c.head_dim != 128) return fail(HALO_EINVAL, "head_dim must be 64 or 128");
     if (c.block_tokens != kBlockTok) return fail(HALO_EINVAL, "block_tokens must be 16");
-    if (c.capacity_blocks < 1 || c.capacity_blocks > (int64_t)kBlkMask ||
+    if (c.capacity_blocks < 1 || c.capacity_blocks * c.num_kv_heads > (int64_t)kBlkMask + 1 ||
         (int64_t)c.num_layers * c.capacity_blocks >= ((int64_t)1 << 31))
         return fail(HALO_EINVAL, "capacity_blocks out of range");
     if ((c.k_storage == nullptr) != (c.v_storage == nullptr))

@@ -77,6 +77,8 @@ struct halo_plan_s {
     std::vector<int32_t> unit_boff, chunk_lo, chunk_u0, chunk_u1, unit_chunk0, unit_nseg, unit_seg;
     int32_t nseg_total = 0;
     std::vector<uint32_t> req_blk;
+    std::vector<uint32_t> k2_ent;     // [Btot][2] K2 block descriptors (PlanDev::k2_ent)
+    std::vector<int32_t> unit_meta;   // [U][8] K2 unit metadata (PlanDev::unit_meta)
     std::vector<halo::PrefixTile> tiles;
     halo_plan_info info{};
     std::vector<uint8_t> host_buf;

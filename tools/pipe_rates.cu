@@ -21,6 +21,10 @@ __global__ void k(float *out, int iters, long long *cyc) {
                            asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(a[(i + 1) & 7]));
                            a[(i+4)&7] = __uint_as_float(u[i] ^ 0x3f800000u); }
             if (OP == 5) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(a[(i+3)&7]));
+            if (OP == 6) { unsigned short lo = (unsigned short)(u[i] + i), hi = (unsigned short)(u[i] >> 3);
+                asm volatile("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(a[i]) : "h"(lo), "h"(hi)); }
+            if (OP == 7) { unsigned w = __float_as_uint(a[(i + 5) & 7]);
+                a[i] += __uint_as_float(w << 16) + __uint_as_float(w & 0xFFFF0000u); }
         }
     }
     long long t1 = clock64();
@@ -31,8 +35,8 @@ __global__ void k(float *out, int iters, long long *cyc) {
 int main() {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     float *out; long long *cyc; cudaMalloc(&out, 1 << 24); cudaMalloc(&cyc, 8);
-    const char *names[] = {"MUFU.EX2 f32", "F2FP f16x2", "FFMA", "FFMA2 (2 flops-pairs)", "MUFU.EX2+F2FP f16 pair", "FMNMX"};
-    for (int op = 0; op < 6; ++op) {
+    const char *names[] = {"MUFU.EX2 f32", "F2FP f16x2", "FFMA", "FFMA2 (2 flops-pairs)", "MUFU.EX2+F2FP f16 pair", "FMNMX", "FHFMA.BF16 (mixed f32<-bf16*bf16)", "bf16x2->2xf32 cvt + 2 FADD"};
+    for (int op = 0; op < 8; ++op) {
         for (int warps : {4, 8, 16}) {
             int iters = 4096;
             auto launch = [&]() {
@@ -42,6 +46,8 @@ int main() {
                 if (op == 3) k<3><<<sms, warps * 32>>>(out, iters, cyc);
                 if (op == 4) k<4><<<sms, warps * 32>>>(out, iters, cyc);
                 if (op == 5) k<5><<<sms, warps * 32>>>(out, iters, cyc);
+                if (op == 6) k<6><<<sms, warps * 32>>>(out, iters, cyc);
+                if (op == 7) k<7><<<sms, warps * 32>>>(out, iters, cyc);
             };
             launch(); cudaDeviceSynchronize();
             launch(); cudaDeviceSynchronize();

@@ -12,7 +12,7 @@ constexpr int kK1Rows = 128;        // K1 tile rows (UMMA M)
 constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
 constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N above this; bounded by smem)
 #ifndef HALO_K2_WARPS
-#define HALO_K2_WARPS 8
+#define HALO_K2_WARPS 12
 #endif
 #ifndef HALO_K2_STAGES
 #define HALO_K2_STAGES 2

@@ -64,15 +64,19 @@ struct Shape {
     static constexpr int LPT = cmax(2, cmax(G, G * D / 64));  // lanes per token row
     static constexpr int TPI = 32 / LPT;                      // tokens per warp iteration
     static constexpr int NIT = kBlockTok / TPI;
-    static constexpr int NCH = D / (8 * LPT);                 // 16-B chunks per lane per row
+    static constexpr int NCH = D / (8 * LPT);                 // 16-B chunks per lane per row (q.k)
+    static constexpr int DPL = D / 32;                        // output dims per lane (P.V)
     static constexpr int SLAB = kBlockTok * D * 2;            // bytes of one (block, head) slab
     static constexpr int STAGE = 2 * SLAB;                    // K + V
     static constexpr int QB = G * D * 2;                      // the unit's q rows (bf16)
-    // ring stages: kStages unless the warps' rings would not fit in 227 KB
-    static constexpr int ST = (kWarps * (kStages * STAGE + 2 * QB + kBlockTok * G * 4 + 256) <= 227 * 1024)
-                                  ? kStages : kStages - 1;
+    // ring stages / q buffers: kStages and 2 unless the warps' rings would not fit in 227 KB
+    static constexpr bool fits(int st, int qn) {
+        return kWarps * (st * STAGE + qn * QB + kBlockTok * G * 4 + 256) <= 227 * 1024;
+    }
+    static constexpr int ST = fits(kStages, 1) ? kStages : kStages - 1;
+    static constexpr int QN = fits(ST, 2) ? 2 : 1;
     static constexpr int OFF_Q = ST * STAGE;
-    static constexpr int OFF_PS = OFF_Q + 2 * QB;
+    static constexpr int OFF_PS = OFF_Q + QN * QB;
     static constexpr int OFF_ALPH = OFF_PS + kBlockTok * G * 4;
     static constexpr int OFF_NT = OFF_ALPH + 8 * 4;
     static constexpr int OFF_BAR = (OFF_NT + ST * 4 + 7) / 8 * 8;
@@ -107,14 +111,47 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[G], int c) {
 }
 
 template <int D, int G>
-using Acc = float2[G][Shape<D, G>::NCH][4];
+using QAcc = float2[G][Shape<D, G>::NCH][4];  // q.k mapping: G heads x this lane's row chunks
+template <int D, int G>
+using OAcc = float2[G][D / 64];               // P.V mapping: G heads x this lane's D/32 dims
+
+// DPL = D/32 consecutive floats at p (16-B or 8-B aligned) <-> float2 pairs
+template <int NP>
+__device__ __forceinline__ void ld_pairs(const float *p, float2 (&x)[NP]) {
+    if constexpr (NP == 2) {
+        const float4 v = *reinterpret_cast<const float4 *>(p);
+        x[0] = make_float2(v.x, v.y);
+        x[1] = make_float2(v.z, v.w);
+    } else {
+        x[0] = *reinterpret_cast<const float2 *>(p);
+    }
+}
+template <int NP>
+__device__ __forceinline__ void ld_pairs_cg(const float *p, float2 (&x)[NP]) {
+    if constexpr (NP == 2) {
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(p));
+        x[0] = make_float2(v.x, v.y);
+        x[1] = make_float2(v.z, v.w);
+    } else {
+        x[0] = __ldcg(reinterpret_cast<const float2 *>(p));
+    }
+}
+template <int NP>
+__device__ __forceinline__ void st_pairs(float *p, const float2 (&x)[NP], float sc) {
+    if constexpr (NP == 2) {
+        *reinterpret_cast<float4 *>(p) = make_float4(x[0].x * sc, x[0].y * sc, x[1].x * sc, x[1].y * sc);
+    } else {
+        *reinterpret_cast<float2 *>(p) = make_float2(x[0].x * sc, x[0].y * sc);
+    }
+}
 
 // Final merge of a unit's suffix state (base-2 max mh, sum lh, unnormalised o) with the
-// request's K1 partials, then the fp32 output / lse store.  Lanes of token group 0 only.
+// request's K1 partials, then the fp32 output / lse store.  All lanes: lane owns dims
+// [lane*D/32, (lane+1)*D/32) of the G heads.
 template <int D, int G>
-__device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head, int nslots, int c,
-                                         const float (&mh)[G], const float (&lh)[G], Acc<D, G> &o2) {
-    using S = Shape<D, G>;
+__device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head, int nslots, int lane,
+                                         const float (&mh)[G], const float (&lh)[G], OAcc<D, G> &o2) {
+    constexpr int NP = D / 64, DPL = D / 32;
     const PlanDev &P = a.p;
     float M[G], L[G];
 #pragma unroll
@@ -130,9 +167,7 @@ __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head,
         const float ws = (lh[h] > 0.f) ? ptx::ex2(mh[h] - M[h]) : 0.f;
         L[h] = lh[h] * ws;
 #pragma unroll
-        for (int k = 0; k < S::NCH; ++k)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) o2[h][k][i] = ptx::fmul2(o2[h][k][i], make_float2(ws, ws));
+        for (int i = 0; i < NP; ++i) o2[h][i] = ptx::fmul2(o2[h][i], make_float2(ws, ws));
     }
     for (int sl = 0; sl < nslots; ++sl) {
 #pragma unroll
@@ -140,28 +175,16 @@ __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head,
             const int64_t row = sl * slot_stride + row0 + h;
             const float w = ptx::ex2(P.part_lse[row] * kLog2e - M[h]);
             L[h] += w;
-            const float2 ww = make_float2(w, w);
+            float2 x[NP];
+            ld_pairs<NP>(P.part_o + row * D + lane * DPL, x);
 #pragma unroll
-            for (int k = 0; k < S::NCH; ++k) {
-                const float4 *po = reinterpret_cast<const float4 *>(P.part_o + row * D + (k * S::LPT + c) * 8);
-                const float4 x0 = po[0], x1 = po[1];
-                o2[h][k][0] = ptx::ffma2(ww, make_float2(x0.x, x0.y), o2[h][k][0]);
-                o2[h][k][1] = ptx::ffma2(ww, make_float2(x0.z, x0.w), o2[h][k][1]);
-                o2[h][k][2] = ptx::ffma2(ww, make_float2(x1.x, x1.y), o2[h][k][2]);
-                o2[h][k][3] = ptx::ffma2(ww, make_float2(x1.z, x1.w), o2[h][k][3]);
-            }
+            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(w, w), x[i], o2[h][i]);
         }
     }
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-        const float inv = 1.f / L[h];
-#pragma unroll
-        for (int k = 0; k < S::NCH; ++k) {
-            float4 *dst = reinterpret_cast<float4 *>(a.out + (row0 + h) * D + (k * S::LPT + c) * 8);
-            dst[0] = make_float4(o2[h][k][0].x * inv, o2[h][k][0].y * inv, o2[h][k][1].x * inv, o2[h][k][1].y * inv);
-            dst[1] = make_float4(o2[h][k][2].x * inv, o2[h][k][2].y * inv, o2[h][k][3].x * inv, o2[h][k][3].y * inv);
-        }
-        if (a.lse != nullptr && c == h) a.lse[row0 + h] = (M[h] + __log2f(L[h])) * kLn2;
+        st_pairs<NP>(a.out + (row0 + h) * D + lane * DPL, o2[h], 1.f / L[h]);
+        if (a.lse != nullptr && lane == h) a.lse[row0 + h] = (M[h] + __log2f(L[h])) * kLn2;
     }
 }
 
@@ -169,6 +192,7 @@ template <int D, int G>
 __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const SuffixArgs a) {
     using S = Shape<D, G>;
     constexpr int LPT = S::LPT, TPI = S::TPI, NIT = S::NIT, NCH = S::NCH, ST = S::ST;
+    constexpr int NP = D / 64, DPL = D / 32;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t *ws = smem_raw + warp * S::WARP_SMEM_AL;
@@ -232,11 +256,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             const uint32_t ex = __shfl_sync(0xffffffffu, ent.x, j);
             const uint32_t ey = __shfl_sync(0xffffffffu, ent.y, j);
             if ((ex >> 31) || px == pstart) {  // first block of a unit in this chunk: its q rows
-                if (q_issued - q_read >= 2) break;  // both q buffers busy
+                if (q_issued - q_read >= (uint32_t)S::QN) break;  // q buffers busy
                 if (lane == 0) {
-                    uint64_t *qb = &qbar[q_issued & 1];
-                    ptx::mbar_arrive_expect_tx(qb, S::QB);
-                    ptx::bulk_g2s(qbuf + (q_issued & 1) * S::QB, a.q + (int64_t)ey * (G * D), S::QB, qb);
+                    const int qi = (int)(q_issued % S::QN);
+                    ptx::mbar_arrive_expect_tx(&qbar[qi], S::QB);
+                    ptx::bulk_g2s(qbuf + qi * S::QB, a.q + (int64_t)ey * (G * D), S::QB, &qbar[qi]);
                 }
                 ++q_issued;
             }
@@ -262,24 +286,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
             const int xs = max(m0.x, lo), xe = min(m0.y, hi);
             const int req = m0.z, head = m0.w;
-            Acc<D, G> o2;
+            OAcc<D, G> o2;
 #pragma unroll
             for (int h = 0; h < G; ++h)
 #pragma unroll
-                for (int k = 0; k < NCH; ++k)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) o2[h][k][i] = make_float2(0.f, 0.f);
+                for (int i = 0; i < NP; ++i) o2[h][i] = make_float2(0.f, 0.f);
             float m = -INFINITY, l = 0.f;
             if (xs < xe) {
                 // q rows of the g heads, this lane's dims, pre-scaled (waits for the bulk copy)
 #if HALO_K2_QK_BF16
                 uint32_t qw[G][NCH][4];  // raw bf16 pairs (scale applied to the score)
 #else
-                Acc<D, G> q2;            // fp32, pre-scaled
+                QAcc<D, G> q2;           // fp32, pre-scaled
 #endif
                 fill();
-                ptx::mbar_wait(&qbar[q_read & 1], (q_read >> 1) & 1);
-                const uint8_t *qs = qbuf + (q_read & 1) * S::QB;
+                ptx::mbar_wait(&qbar[q_read % S::QN], (q_read / S::QN) & 1);
+                const uint8_t *qs = qbuf + (q_read % S::QN) * S::QB;
 #pragma unroll
                 for (int h = 0; h < G; ++h)
 #pragma unroll
@@ -367,9 +389,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                         for (int h = 0; h < G; ++h) {
                             const float al = alph[h];
 #pragma unroll
-                            for (int k = 0; k < NCH; ++k)
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) o2[h][k][i] = ptx::fmul2(o2[h][k][i], make_float2(al, al));
+                            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::fmul2(o2[h][i], make_float2(al, al));
                         }
                     }
 #pragma unroll
@@ -382,34 +402,39 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                         for (int it = 0; it < NIT; ++it) ps[(it * TPI + tg) * G + hsel] = s[it];
                     }
                     __syncwarp();
-                    // ---- o += P.V ----
+                    // ---- o += P.V: lane owns dims [lane*DPL, +DPL) of all G heads ----
+                    auto pv_token = [&](int t) {
+                        float p[G];
+                        if constexpr (G % 4 == 0) {
 #pragma unroll
-                    for (int it = 0; it < NIT; ++it) {
-                        const int t = it * TPI + tg;
-                        if (t < ntok) {
-                            float p[G];
-                            if constexpr (G % 4 == 0) {
-#pragma unroll
-                                for (int h4 = 0; h4 < G; h4 += 4) {
-                                    const float4 p4 = *reinterpret_cast<const float4 *>(ps + t * G + h4);
-                                    p[h4] = p4.x; p[h4 + 1] = p4.y; p[h4 + 2] = p4.z; p[h4 + 3] = p4.w;
-                                }
-                            } else {
-#pragma unroll
-                                for (int h = 0; h < G; ++h) p[h] = ps[t * G + h];
+                            for (int h4 = 0; h4 < G; h4 += 4) {
+                                const float4 p4 = *reinterpret_cast<const float4 *>(ps + t * G + h4);
+                                p[h4] = p4.x; p[h4 + 1] = p4.y; p[h4 + 2] = p4.z; p[h4 + 3] = p4.w;
                             }
-#pragma unroll
-                            for (int k = 0; k < NCH; ++k) {
-                                const uint4 raw = *reinterpret_cast<const uint4 *>(vb + t * (D * 2) + (k * LPT + c) * 16);
-                                const float2 v[4] = {ptx::bf2_to_f2(raw.x), ptx::bf2_to_f2(raw.y),
-                                                     ptx::bf2_to_f2(raw.z), ptx::bf2_to_f2(raw.w)};
-#pragma unroll
-                                for (int h = 0; h < G; ++h)
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i)
-                                        o2[h][k][i] = ptx::ffma2(make_float2(p[h], p[h]), v[i], o2[h][k][i]);
-                            }
+                        } else if constexpr (G == 2) {
+                            const float2 p2 = *reinterpret_cast<const float2 *>(ps + t * 2);
+                            p[0] = p2.x; p[1] = p2.y;
+                        } else {
+                            p[0] = ps[t];
                         }
+                        float2 v[NP];
+                        if constexpr (NP == 2) {
+                            const uint2 raw = *reinterpret_cast<const uint2 *>(vb + t * (D * 2) + lane * 8);
+                            v[0] = ptx::bf2_to_f2(raw.x);
+                            v[1] = ptx::bf2_to_f2(raw.y);
+                        } else {
+                            v[0] = ptx::bf2_to_f2(*reinterpret_cast<const uint32_t *>(vb + t * (D * 2) + lane * 4));
+                        }
+#pragma unroll
+                        for (int h = 0; h < G; ++h)
+#pragma unroll
+                            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(p[h], p[h]), v[i], o2[h][i]);
+                    };
+                    if (ntok == kBlockTok) {
+#pragma unroll
+                        for (int t = 0; t < kBlockTok; ++t) pv_token(t);
+                    } else {
+                        for (int t = 0; t < ntok; ++t) pv_token(t);
                     }
                     __syncwarp();
                     ++c_count;
@@ -417,20 +442,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 fill();
             }
 
-            // ---- combine the TPI token groups ----
+            // ---- combine l over the TPI token groups (o is already per dim) ----
 #pragma unroll
-            for (int msk = LPT; msk < 32; msk <<= 1) {
-                l += __shfl_xor_sync(0xffffffffu, l, msk);
-#pragma unroll
-                for (int h = 0; h < G; ++h)
-#pragma unroll
-                    for (int k = 0; k < NCH; ++k)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            o2[h][k][i].x += __shfl_xor_sync(0xffffffffu, o2[h][k][i].x, msk);
-                            o2[h][k][i].y += __shfl_xor_sync(0xffffffffu, o2[h][k][i].y, msk);
-                        }
-            }
+            for (int msk = LPT; msk < 32; msk <<= 1) l += __shfl_xor_sync(0xffffffffu, l, msk);
             // per-head (m, l) from the lane that owns each head
             float mh[G], lh[G];
 #pragma unroll
@@ -440,21 +454,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             }
             const int nslots = m1.x, nseg = m1.y;
             if (nseg == 1) {
-                if (tg == 0) finalize<D, G>(a, req, head, nslots, c, mh, lh, o2);
+                finalize<D, G>(a, req, head, nslots, lane, mh, lh, o2);
             } else {
                 // ---- stream-K: publish this piece's state; the last piece merges them all ----
                 const int slot = m1.z + (cc - m1.w);
-                if (tg == 0) {
 #pragma unroll
-                    for (int h = 0; h < G; ++h)
+                for (int h = 0; h < G; ++h) st_pairs<NP>(P.seg_o + ((int64_t)slot * G + h) * D + lane * DPL, o2[h], 1.f);
 #pragma unroll
-                        for (int k = 0; k < NCH; ++k) {
-                            float4 *dst = reinterpret_cast<float4 *>(P.seg_o + ((int64_t)slot * G + h) * D + (k * LPT + c) * 8);
-                            dst[0] = make_float4(o2[h][k][0].x, o2[h][k][0].y, o2[h][k][1].x, o2[h][k][1].y);
-                            dst[1] = make_float4(o2[h][k][2].x, o2[h][k][2].y, o2[h][k][3].x, o2[h][k][3].y);
-                        }
-                    if (c < G) *reinterpret_cast<float2 *>(P.seg_ml + ((int64_t)slot * G + c) * 2) = make_float2(mh[c], lh[c]);
-                }
+                for (int h = 0; h < G; ++h)
+                    if (lane == h) *reinterpret_cast<float2 *>(P.seg_ml + ((int64_t)slot * G + h) * 2) = make_float2(mh[h], lh[h]);
                 __threadfence();
                 __syncwarp();
                 int old = 0;
@@ -463,44 +471,34 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 if (old == nseg - 1) {
                     __threadfence();
                     if (lane == 0) P.unit_count[u] = 0;  // ready for the next launch
-                    if (tg == 0) {
-                        // merge all pieces in segment order (deterministic), from L2
-                        float M[G], L[G];
+                    // merge all pieces in segment order (deterministic), from L2
+                    float M[G], L[G];
 #pragma unroll
-                        for (int h = 0; h < G; ++h) { M[h] = -INFINITY; L[h] = 0.f; }
-                        const int base = m1.z;
-                        for (int sg = 0; sg < nseg; ++sg)
-#pragma unroll
-                            for (int h = 0; h < G; ++h)
-                                M[h] = fmaxf(M[h], __ldcg(P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
+                    for (int h = 0; h < G; ++h) { M[h] = -INFINITY; L[h] = 0.f; }
+                    const int base = m1.z;
+                    for (int sg = 0; sg < nseg; ++sg)
 #pragma unroll
                         for (int h = 0; h < G; ++h)
+                            M[h] = fmaxf(M[h], __ldcg(P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
 #pragma unroll
-                            for (int k = 0; k < NCH; ++k)
+                    for (int h = 0; h < G; ++h)
 #pragma unroll
-                                for (int i = 0; i < 4; ++i) o2[h][k][i] = make_float2(0.f, 0.f);
-                        for (int sg = 0; sg < nseg; ++sg) {
+                        for (int i = 0; i < NP; ++i) o2[h][i] = make_float2(0.f, 0.f);
+                    for (int sg = 0; sg < nseg; ++sg) {
 #pragma unroll
-                            for (int h = 0; h < G; ++h) {
-                                const float2 ml = __ldcg(reinterpret_cast<const float2 *>(
-                                    P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
-                                const float w = (ml.y > 0.f) ? ptx::ex2(ml.x - M[h]) : 0.f;
-                                L[h] += ml.y * w;
-                                const float2 ww = make_float2(w, w);
+                        for (int h = 0; h < G; ++h) {
+                            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(
+                                P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
+                            const float w = (ml.y > 0.f) ? ptx::ex2(ml.x - M[h]) : 0.f;
+                            L[h] += ml.y * w;
+                            float2 x[NP];
+                            ld_pairs_cg<NP>(P.seg_o + ((int64_t)(base + sg) * G + h) * D + lane * DPL, x);
 #pragma unroll
-                                for (int k = 0; k < NCH; ++k) {
-                                    const float4 *src = reinterpret_cast<const float4 *>(
-                                        P.seg_o + ((int64_t)(base + sg) * G + h) * D + (k * LPT + c) * 8);
-                                    const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-                                    o2[h][k][0] = ptx::ffma2(ww, make_float2(x0.x, x0.y), o2[h][k][0]);
-                                    o2[h][k][1] = ptx::ffma2(ww, make_float2(x0.z, x0.w), o2[h][k][1]);
-                                    o2[h][k][2] = ptx::ffma2(ww, make_float2(x1.x, x1.y), o2[h][k][2]);
-                                    o2[h][k][3] = ptx::ffma2(ww, make_float2(x1.z, x1.w), o2[h][k][3]);
-                                }
-                            }
+                            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(w, w), x[i], o2[h][i]);
                         }
-                        finalize<D, G>(a, req, head, nslots, c, M, L, o2);
                     }
+                    finalize<D, G>(a, req, head, nslots, lane, M, L, o2);
+
                 }
             }
             __syncwarp();

@@ -36,6 +36,7 @@ METRIC = "shared-prefix decode attn queries/s; HBM GB/s & TC util vs peak; KV mi
 UNIT = "queries/s"
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
 FALLBACK_BF16_TFLOPS = 1590.0
+NVLINK_PEER_GBS = 770.0     # B200_PROFILING.md: measured peer copy per direction
 
 
 def peaks():
@@ -188,38 +189,11 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU leg
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="halo", choices=["halo", "reference"])
-    ap.add_argument("--config", default="fanout")
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle time")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-migration", action="store_true")
-    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
-        return run_reference(args)
-
-    import torch
-    import torch.distributed as dist
-    import paper_2509_02121_b200 as halo
+def setup_workload(halo, wl, dev, torch):
+    """Load `wl` into a fresh pool (inputs resident in HBM), append this step's token, plan.
+    Returns the loaded pool, the plan, its info and the step closure."""
     from paper_2509_02121_b200.loader import blocks_needed, load
-    from synth import make_config
-
-    rank, world, local = dist_env()
-    dev = local
-    torch.cuda.set_device(dev)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
-    halo.load_library()
-
-    wl = make_config(args.config, seed=1 + 1000 * rank)
-    L, R, Hq, Hkv, D = wl.layers, wl.nreq, wl.hq, wl.hkv, wl.d
+    L, R, Hq, D = wl.layers, wl.nreq, wl.hq, wl.d
     ld = load(wl, dev, capacity=blocks_needed(wl, steps=2, slack=4096))
     pool, reqs = ld.pool, ld.req_ids
     nk, nv = wl.new_kv(0, f"cuda:{dev}")            # [L][R][Hkv][D] this step's token
@@ -246,22 +220,33 @@ def main():
             plan.run_stages(l, 2, q[l], out[l], lse[l])
             if evs is not None:
                 evs[l][2].record(stream)
+    return ld, plan, info, step, (nk, nv, q, out, lse, ones, popt)
 
-    for _ in range(args.warmup):
+
+def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=False):
+    """W untimed steps, then K timed steps between barriers + syncs (CUDA events on the
+    launching stream); per-kernel times from events around each K1 / K2 launch.  Max over
+    ranks."""
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)]
-           for _ in range(args.steps)]
+           for _ in range(steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev) as clk:
-        t_start.record(stream)
-        for s in range(args.steps):
-            step(evs[s])
-        t_end.record(stream)
-        torch.cuda.synchronize()
+    clk = ClockSampler(dev) if sample_clocks else None
+    if clk:
+        clk.__enter__()
+    t_start.record(stream)
+    for s in range(steps):
+        step(evs[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
@@ -271,15 +256,97 @@ def main():
         t = torch.tensor([ms, k1_ms, k2_ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, k1_ms, k2_ms = t.tolist()
+    return ms, k1_ms, k2_ms, clk
+
+
+def kernel_rooflines(info, k1_launch_ms, k2_launch_ms):
+    hbm_peak, tc_peak, _, peak_src = peaks()
+    k2_gbs = info["k2_bytes"] / (k2_launch_ms * 1e-3) / 1e9
+    k1_tflops = info["k1_flops"] / (k1_launch_ms * 1e-3) / 1e12 if info["k1_flops"] else None
+    return ({"bound": "hbm", "kernel": "suffix_decode_kernel (K2+K3)", "achieved": k2_gbs,
+             "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
+             "algorithmic_bytes_per_launch": info["k2_bytes"], "avg_launch_ms": k2_launch_ms,
+             "peak_source": peak_src},
+            {"bound": "tensor", "kernel": "prefix_attn_kernel (K1)", "achieved": k1_tflops,
+             "peak": tc_peak, "unit": "TFLOP/s", "frac": (k1_tflops / tc_peak) if k1_tflops else None,
+             "algorithmic_flops_per_launch": info["k1_flops"], "avg_launch_ms": k1_launch_ms,
+             "peak_source": peak_src})
+
+
+def measure_other_configs(halo, names, layers, steps, warmup, world, dev, torch, dist):
+    """Per-launch K1/K2 rooflines on the other BASELINE configs (C2 tree, C3 analytics per
+    GPU) with `layers` layers: same kernels and plan as C1; the per-layer work (and so the
+    per-launch rooflines) is that of the full 32-layer config."""
+    from synth import make_config
+    res = {}
+    for name in names:
+        wl = make_config(name, layers=layers)
+        ld, plan, info, step, bufs = setup_workload(halo, wl, dev, torch)
+        ms, k1_ms, k2_ms, _ = time_steps(step, wl.layers, steps, warmup, world, dev, torch, dist)
+        n = steps * wl.layers
+        k2r, k1r = kernel_rooflines(info, k1_ms / n, k2_ms / n)
+        layer_ms = (k1_ms + k2_ms) / n
+        res[name] = {"requests": wl.nreq, "layers_run": wl.layers,
+                     "prefix_nodes": len(wl.nodes), "k1_tiles": info["k1_tiles"],
+                     "k2_units": info["k2_units"], "layer_ms": layer_ms,
+                     "queries_per_s_kernels": wl.nreq / (layer_ms * 1e-3),
+                     "roofline": k2r, "prefix_roofline": k1r,
+                     "unshared_bytes_per_layer": info["unshared_bytes"]}
+        plan.destroy()
+        ld.pool.destroy()
+        del bufs, step
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="halo", choices=["halo", "reference"])
+    ap.add_argument("--config", default="fanout")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle time")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-migration", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--other-configs", default="tree,analytics",
+                    help="BASELINE configs also measured per launch (C2 tree, C3 analytics); '' = none")
+    ap.add_argument("--other-layers", type=int, default=4)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2509_02121_b200 as halo
+    from paper_2509_02121_b200.loader import blocks_needed, load
+    from synth import make_config
+
+    rank, world, local = dist_env()
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    halo.load_library()
+
+    wl = make_config(args.config, seed=1 + 1000 * rank)
+    L, R, Hq, Hkv, D = wl.layers, wl.nreq, wl.hq, wl.hkv, wl.d
+    ld, plan, info, step, (nk, nv, q, out, lse, ones, popt) = setup_workload(halo, wl, dev, torch)
+    pool, reqs = ld.pool, ld.req_ids
+    stream = torch.cuda.current_stream()
+    ms, k1_ms, k2_ms, clk = time_steps(step, L, args.steps, args.warmup, world, dev, torch, dist,
+                                       sample_clocks=True)
     launches = args.steps * (1 + 2 * L)
     ms_step = ms / args.steps
     value = R * L * world * args.steps / (ms / 1e3)
 
-    hbm_peak, tc_peak, tc_sustained, peak_src = peaks()
     k2_launch_ms = k2_ms / (args.steps * L)
     k1_launch_ms = k1_ms / (args.steps * L)
-    k2_gbs = info["k2_bytes"] / (k2_launch_ms * 1e-3) / 1e9
-    k1_tflops = info["k1_flops"] / (k1_launch_ms * 1e-3) / 1e12 if info["k1_flops"] else None
+    k2_roof, k1_roof = kernel_rooflines(info, k1_launch_ms, k2_launch_ms)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -321,6 +388,11 @@ def main():
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
         extra["migration"] = measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist)
+    # ---- per-launch rooflines on the other configs (C2, C3) ----
+    if args.other_configs and not args.profile:
+        extra["other_configs"] = measure_other_configs(
+            halo, [x for x in args.other_configs.split(",") if x], args.other_layers,
+            max(3, min(args.steps, 10)), 3, world, dev, torch, dist)
     # ---- CPU oracle baseline ----
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         n, t, cores = oracle_sample(wl, args.cpu_budget)
@@ -341,16 +413,8 @@ def main():
                        "parallelism": f"request-group sharding x{world} (no collective)",
                        "l2": "inputs exceed L2 (8.3 GiB KV touched per step vs 126 MB L2)",
                        "k1_tiles": info["k1_tiles"], "k2_units": info["k2_units"]},
-            "roofline": {"bound": "hbm", "kernel": "suffix_decode_kernel (K2+K3)",
-                         "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": k2_gbs / hbm_peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": info["k2_bytes"],
-                         "avg_launch_ms": k2_launch_ms, "peak_source": peak_src},
-            "prefix_roofline": {"bound": "tensor", "kernel": "prefix_attn_kernel (K1)",
-                                "achieved": k1_tflops, "peak": tc_peak, "unit": "TFLOP/s",
-                                "frac": (k1_tflops / tc_peak) if k1_tflops else None,
-                                "algorithmic_flops_per_launch": info["k1_flops"],
-                                "avg_launch_ms": k1_launch_ms, "peak_source": peak_src},
+            "roofline": dict(k2_roof, traffic=traffic),
+            "prefix_roofline": k1_roof,
             "step_breakdown_ms": {"k1": k1_ms / args.steps, "k2": k2_ms / args.steps,
                                   "other": ms_step - (k1_ms + k2_ms) / args.steps},
             "unshared_bytes_per_layer": info["unshared_bytes"],
@@ -366,26 +430,61 @@ def main():
 
 
 def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):
+    """K4 / relocation copies of the C1 template node (2048 tokens x 32 layers x 8 heads =
+    256 MiB of K+V).  Every copy is timed with CUDA events on the launching stream after two
+    warm-up calls; HBM roofline = (read + write bytes) / time vs the measured copy peak.
+    N=1: pack (K4 gather to the exchange layout, halo_prefix_read), unpack (registration
+    from a device exchange buffer, halo_prefix_register), and same-GPU relocation
+    (halo_prefix_clone: pool-to-pool whole-block copy).  N>1: NCCL send/recv rank0 -> rank1."""
     node = ld.node_ids[0]
     ntok = wl.nodes[0].ntok
     nbytes = ntok * wl.layers * wl.hkv * wl.d * 2 * 2
-    if world == 1:
-        dst = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, (ntok + 15) // 16 * 3, dev)
+    hbm_peak = peaks()[0]
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps=3):
         for _ in range(2):
-            n = pool.clone_prefix(node, dst, -1)
-            torch.cuda.synchronize()
-            dst.release_prefix(n)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        n = pool.clone_prefix(node, dst, -1)
-        e1.record()
+            fn()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        dst.release_prefix(n)
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        return best
+
+    def entry(ms, what):
+        return {"what": what, "bytes": nbytes, "ms": ms, "GB/s": nbytes / ms / 1e6,
+                "hbm_roofline": {"bound": "hbm", "achieved": 2 * nbytes / ms / 1e6, "peak": hbm_peak,
+                                 "unit": "GB/s", "frac": 2 * nbytes / ms / 1e6 / hbm_peak}}
+
+    if world == 1:
+        res = {"mode": "N=1: no NCCL; K4 pack, K4 unpack and same-GPU relocation timed separately"}
+        kx = torch.empty((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
+        vx = torch.empty_like(kx)
+        ms = timed(lambda: pool.read_prefix(node, kx, vx, stream))
+        res["pack"] = entry(ms, "K4 gather: pool blocks -> exchange layout [layer][token][head][d]")
+        dst = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, (ntok + 15) // 16 * 4, dev)
+
+        def unpack():
+            n = dst.register_prefix(-1, ntok, kx, vx, stream)
+            dst.release_prefix(n)
+        ms = timed(unpack)
+        res["unpack"] = entry(ms, "K4 scatter: exchange layout -> fresh pool blocks (register)")
+
+        def clone():
+            n = pool.clone_prefix(node, dst, -1, stream)
+            dst.release_prefix(n)
+        ms = timed(clone)
+        res["relocate"] = entry(ms, "same-GPU relocation: pool-to-pool whole-block copy")
+        torch.cuda.synchronize()
         dst.destroy()
-        return {"mode": "same-GPU relocation through K4 pack+unpack (no NCCL at N=1)",
-                "bytes": nbytes, "ms": ms, "GB/s": nbytes / ms / 1e6,
-                "hbm_bytes": 4 * nbytes, "hbm_GB/s": 4 * nbytes / ms / 1e6}
+        del kx, vx
+        return res
     uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
     obj = [uid]
     dist.broadcast_object_list(obj, src=0)
@@ -407,8 +506,13 @@ def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         if newn is not None:
             pool.release_prefix(newn)
+        gbs = nbytes / ms.item() / 1e6
         res = {"mode": "rank0 -> rank1 NCCL send/recv (COPY), K4 pack/unpack pipelined",
-               "bytes": nbytes, "ms": ms.item(), "GB/s": nbytes / ms.item() / 1e6}
+               "bytes": nbytes, "ms": ms.item(), "GB/s": gbs,
+               "nvlink_roofline": {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_PEER_GBS,
+                                   "unit": "GB/s", "frac": gbs / NVLINK_PEER_GBS,
+                                   "peak_source": "measured peer copy per direction "
+                                                  "(B200_PROFILING.md; 900 nominal)"}}
     return res
 
 

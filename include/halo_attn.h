@@ -222,8 +222,11 @@ halo_status halo_migrate_send(halo_pool pool, int64_t node, int32_t dst_rank, in
  * `parent` (-1 = root).  ncclRecv pipelined with the K4 unpack kernel. */
 halo_status halo_migrate_recv(halo_pool pool, int32_t src_rank, int64_t parent, int32_t ntok,
                               void *stream, int64_t *node_out);
-/* Same-device relocation: pack `node` of `src` and unpack it into `dst` (which may be the
- * same pool) under `parent_dst`, through the same chunked K4 path as a migration. */
+/* Same-device relocation ("cache snapshots ... migrated"): copy `node` of
+ * `src` into fresh blocks of `dst` (which may be the same pool; same device and KV
+ * geometry, EINVAL otherwise) under `parent_dst`.  One whole-block pool-to-pool copy
+ * kernel: a (layer, block) of all heads is contiguous on both sides.  Stream-ordered on
+ * `stream`; ENOMEM leaves dst unchanged. */
 halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_t parent_dst,
                               void *stream, int64_t *node_out);
 

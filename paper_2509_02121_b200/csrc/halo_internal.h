@@ -97,4 +97,12 @@ cudaError_t launch_kv_gather(const PoolGeom &g, const void *pool_k, const void *
                              void *dst_k, void *dst_v, const int32_t *slots, int64_t n,
                              int layer_begin, int layer_end, int num_sms, cudaStream_t s);
 
+// Same-device relocation: pool block pairs[2i] -> destination block pairs[2i+1], all
+// layers in [layer_begin, layer_end), K and V (whole blocks: a partial block's zero tail
+// is copied as well).
+cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const void *src_v,
+                                  const PoolGeom &dg, void *dst_k, void *dst_v,
+                                  const int32_t *pairs, int32_t nblk, int layer_begin,
+                                  int layer_end, int num_sms, cudaStream_t s);
+
 }  // namespace halo

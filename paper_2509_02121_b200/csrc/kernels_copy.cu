@@ -131,7 +131,54 @@ void shape(const PoolGeom &pg, int64_t n, int layers, int num_sms, Geo &g, dim3 
     grid = dim3((unsigned)want, (unsigned)layers, 1);
 }
 
+// Pool-to-pool block copy (same device): pair i copies pool block src_blk[i] of every
+// layer in [layer_begin, layer_end) to block dst_blk[i] of the destination pool, K and V.
+// A (layer, block) of all heads is one contiguous run of hkv*16*d*2 bytes on both sides
+// (32 KiB at hkv=8, d=128), so this is a plain streaming copy: 16-B loads, kCopyUnroll in
+// flight per thread, the grid a multiple of the SM count.
+constexpr int kCopyUnroll = 8;
+__global__ void __launch_bounds__(256) kv_copy_blocks_kernel(
+    const int4 *__restrict__ sk, const int4 *__restrict__ sv, int4 *__restrict__ dk,
+    int4 *__restrict__ dv, const int32_t *__restrict__ pairs, int64_t nitems, int32_t nblk,
+    int32_t run16, int64_t src_layer16, int64_t dst_layer16, int layer_begin) {
+    // item = ((layer - layer_begin) * nblk + pair) * 2 + (K|V): one contiguous run of run16 int4
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int kv = (int)(item & 1);
+        const int64_t lp = item >> 1;
+        const int32_t pr = (int32_t)(lp % nblk);
+        const int64_t layer = layer_begin + lp / nblk;
+        const int4 *src = (kv ? sv : sk) + layer * src_layer16 + (int64_t)pairs[2 * pr] * run16;
+        int4 *dst = (kv ? dv : dk) + layer * dst_layer16 + (int64_t)pairs[2 * pr + 1] * run16;
+        for (int o0 = threadIdx.x; o0 < run16; o0 += 256 * kCopyUnroll) {
+            int4 v[kCopyUnroll];
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u)
+                if (o0 + u * 256 < run16) v[u] = ld_stream(src + o0 + u * 256);
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u)
+                if (o0 + u * 256 < run16) dst[o0 + u * 256] = v[u];
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const void *src_v,
+                                  const PoolGeom &dg, void *dst_k, void *dst_v,
+                                  const int32_t *pairs, int32_t nblk, int layer_begin,
+                                  int layer_end, int num_sms, cudaStream_t s) {
+    const int layers = layer_end - layer_begin;
+    if (nblk == 0 || layers <= 0) return cudaSuccess;
+    const int32_t run16 = sg.hkv * kBlockTok * sg.d * 2 / 16;  // int4 chunks per (layer, block)
+    const int64_t nitems = (int64_t)layers * nblk * 2;
+    int64_t grid = nitems;
+    const int64_t cap = (int64_t)num_sms * 8;  // 8 CTAs of 256 threads per SM
+    if (grid > cap) grid = cap;
+    kv_copy_blocks_kernel<<<(unsigned)grid, 256, 0, s>>>(
+        (const int4 *)src_k, (const int4 *)src_v, (int4 *)dst_k, (int4 *)dst_v, pairs, nitems,
+        nblk, run16, sg.cap * run16, dg.cap * run16, layer_begin);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_kv_scatter(const PoolGeom &pg, void *pool_k, void *pool_v, const void *src_k,
                               const void *src_v, int64_t src_rows, const int32_t *slots,

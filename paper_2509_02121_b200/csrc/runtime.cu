@@ -828,6 +828,21 @@ halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
             return fail(HALO_EINVAL, "no CUDA device %d", c.device);
         }
         cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+        {
+            // The library's small per-call device scratch (slot lists, block pairs) comes from
+            // cudaMallocAsync; keep up to 1 GiB of freed memory cached in the device's default
+            // pool instead of unmapping it at every synchronisation (release threshold 0).
+            cudaMemPool_t mp;
+            if (cudaDeviceGetDefaultMemPool(&mp, c.device) == cudaSuccess) {
+                uint64_t thr = 0;
+                cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+                if (thr < (1ull << 30)) {
+                    thr = 1ull << 30;
+                    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
+            }
+            cudaGetLastError();
+        }
         const size_t bytes = storage_bytes(c);
         if (c.k_storage) {
             p->k = c.k_storage;
@@ -1463,28 +1478,17 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
     std::vector<int32_t> blocks;
     halo_status st = alloc_blocks(dst, nblk, blocks);
     if (st != HALO_OK) return st;
-    const int L = src->cfg.num_layers, lpc = layers_per_chunk(src, ntok);
-    const size_t layer_bytes = (size_t)ntok * src->cfg.num_kv_heads * src->cfg.head_dim * 2;
-    std::vector<int32_t> sslots = token_slots(it->second.blocks, ntok);
-    std::vector<int32_t> dslots = token_slots(blocks, nblk * kBlockTok);
-    Scratch s1, s2, buf;
-    if ((st = upload(sslots.data(), sslots.size() * 4, s, s1)) == HALO_OK &&
-        (st = upload(dslots.data(), dslots.size() * 4, s, s2)) == HALO_OK) {
-        buf.s = s;
-        if (cudaMallocAsync(&buf.ptr, 2 * lpc * layer_bytes, s) != cudaSuccess) {
-            cudaGetLastError();
-            st = fail(HALO_ENOMEM, "staging allocation failed");
-        }
+    // whole-block pool-to-pool copy: a (layer, block) of all heads is contiguous on both sides
+    std::vector<int32_t> pairs(2 * nblk);
+    for (int64_t b = 0; b < nblk; ++b) {
+        pairs[2 * b] = it->second.blocks[b];
+        pairs[2 * b + 1] = blocks[b];
     }
-    for (int l0 = 0; st == HALO_OK && l0 < L; l0 += lpc) {
-        const int l1 = std::min(L, l0 + lpc);
-        uint8_t *b = static_cast<uint8_t *>(buf.ptr);
-        const size_t half = (size_t)(l1 - l0) * layer_bytes;
-        cudaError_t e = launch_kv_gather(src->geom, src->k, src->v, b, b + half, (const int32_t *)s1.ptr, ntok, l0, l1,
-                                         src->num_sms, s);
-        if (e == cudaSuccess)
-            e = launch_kv_scatter(dst->geom, dst->k, dst->v, b, b + half, ntok, (const int32_t *)s2.ptr, ntok,
-                                  nblk * kBlockTok - ntok, l0, l1, dst->num_sms, s);
+    Scratch sp;
+    if ((st = upload(pairs.data(), pairs.size() * 4, s, sp)) == HALO_OK) {
+        cudaError_t e = launch_kv_copy_blocks(src->geom, src->k, src->v, dst->geom, dst->k, dst->v,
+                                              (const int32_t *)sp.ptr, (int32_t)nblk, 0,
+                                              src->cfg.num_layers, src->num_sms, s);
         if (e != cudaSuccess) st = fail(HALO_ECUDA, "clone launch: %s", cudaGetErrorString(e));
     }
     if (st != HALO_OK) {

@@ -252,10 +252,9 @@ def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=Fa
     ms = t_start.elapsed_time(t_end)
     k1_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st)
     k2_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st)
-    if world > 1:
-        t = torch.tensor([ms, k1_ms, k2_ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, k1_ms, k2_ms = t.tolist()
+    from paper_2509_02121_b200.sharding import max_over_ranks
+    ms, k1_ms, k2_ms = max_over_ranks([ms, k1_ms, k2_ms], dist if world > 1 else None,
+                                      f"cuda:{dev}")
     return ms, k1_ms, k2_ms, clk
 
 

@@ -314,6 +314,7 @@ def main():
     ap.add_argument("--other-configs", default="tree,analytics",
                     help="BASELINE configs also measured per launch (C2 tree, C3 analytics); '' = none")
     ap.add_argument("--other-layers", type=int, default=4)
+    ap.add_argument("--layers", type=int, default=0, help="override the config's layer count (profiling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -332,7 +333,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     halo.load_library()
 
-    wl = make_config(args.config, seed=1 + 1000 * rank)
+    wl = make_config(args.config, seed=1 + 1000 * rank, **({"layers": args.layers} if args.layers else {}))
     L, R, Hq, Hkv, D = wl.layers, wl.nreq, wl.hq, wl.hkv, wl.d
     ld, plan, info, step, (nk, nv, q, out, lse, ones, popt) = setup_workload(halo, wl, dev, torch)
     pool, reqs = ld.pool, ld.req_ids

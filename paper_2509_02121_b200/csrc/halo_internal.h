@@ -8,7 +8,7 @@
 namespace halo {
 
 constexpr int kBlockTok = 16;       // tokens per KV block
-constexpr int kK1Rows = 128;        // K1 tile rows (UMMA M)
+constexpr int kK1Rows = 256;        // K1 tile rows (two UMMA M=128 sub-tiles)
 constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
 constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N above this; bounded by smem)
 #ifndef HALO_K2_WARPS

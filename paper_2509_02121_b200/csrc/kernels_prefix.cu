@@ -10,24 +10,28 @@
 // K3 (fused into K2) merges with the private suffix -> identical to unshared attention
 // ("Exact answers").
 //
-// Per CTA = one tile: 128 query rows (UMMA M) x a token range of the node (split-N).
-//   warps 0-7   two softmax warpgroups; warp w owns TMEM lanes 32*(w%4).. (rows) and
-//               column half w/4 of every S tile.  Each thread: thread i owns row i (TMEM lane i): tcgen05.ld of its
-//               64 scores, row max (halves exchanged through smem), exp2 / row sum in
-//               registers, P packed to 16-bit pairs and written to TMEM with tcgen05.st (no
-//               smem traffic), lazy O rescale (only when the running max grows by > 2^8),
-//               final normalisation.  Two warps per SMSP hide each other's latencies.
-//   warp 8      TMA producer: two independent rings (K and V, 3 stages each); a 128-token
-//               tile = 8 paged 16-token blocks, one 4-D TMA box per (block, 64-wide d atom),
-//               128-B swizzle.  K stages free after Q.K^T, V stages after P.V.
-//   warp 9      TMEM allocator (512 columns) + MMA issuer (one thread):
-//               S_b = Q K^T (SS, double-buffered S0/S1), O += P V (A = P from TMEM).
-//   warps 10-11 V converters (fp16-P mode): bf16 -> fp16 in place on each V stage, so the
-//               P.V MMA runs with fp16 operands (P in fp16 is 8x more precise than bf16;
-//               kind::f16 needs A and B in the same format).
-
-// TMEM columns: S0 [0,128) | S1 [128,256) | O [256,256+d) | P0 [384,448) | P1 [448,512).
-// Issue order QK(0) QK(1) PV(0) QK(2) PV(1) ... : QK(n+1) runs while softmax works on S(n).
+// Per CTA = one tile: 256 query rows as two UMMA M=128 sub-tiles A and B sharing every K/V
+// stage (half the smem/TMA traffic per FLOP of a 128-row tile), x a token range of the
+// node (split-N), 128-token n-tiles.
+//   warps 0-3   softmax warpgroup A, warps 4-7 softmax warpgroup B: thread = one query row
+//               of its sub-tile (= its TMEM lane), the full 128-column score row per n-tile,
+//               so row max / row sum need no cross-thread exchange.  Online softmax in base
+//               2 with a lazy reference max: p = 2^(s*c - m_ref) is computed optimistically
+//               with the current m_ref (packed to fp16 pairs in registers) and only if some
+//               row's max exceeds m_ref + 8 does the warp rescale O in TMEM and redo the
+//               tile.  P is written with tcgen05.st over the sub-tile's own S columns.
+//   warp 8      TMA producer: K ring (kSK stages) and V ring (kSV stages) of 128-token tiles
+//               = 8 paged 16-token blocks (one 4-D box per 128-token run of physically
+//               consecutive blocks, else one per block), 128-B swizzle.
+//   warp 9      TMEM allocator (512 columns) + MMA issuer (one thread), ping-pong order
+//                  PV_A(n-1) QK_A(n) PV_B(n-1) QK_B(n)
+//               so softmax A(n) overlaps PV_B(n-1) + QK_B(n) on the tensor pipe and vice
+//               versa.  tcgen05.mma executes in issue order, so QK_X(n) may overwrite the
+//               S/P columns PV_X(n-1) reads.
+//   warps 10-11 V converters: bf16 -> fp16 in place on each V stage (fp16 P needs fp16 V:
+//               kind::f16 takes A and B in one format; reading R8).
+//
+// TMEM columns: S_A/P_A [0,128) | S_B/P_B [128,256) | O_A [256,256+d) | O_B [384,384+d).
 #include "halo_internal.h"
 #include "ptx.h"
 
@@ -35,7 +39,7 @@
 
 #ifdef HALO_K1_TRACE
 // Debug timeline of CTA 0: g_k1_trace[event * 64 + tile] = %globaltimer (ns).
-__device__ unsigned long long *g_k1_trace = nullptr;  // [12][64]
+__device__ unsigned long long *g_k1_trace = nullptr;  // [16][64]
 #define K1_TRACE(ev, n)                                                                 \
     do {                                                                                \
         if (blockIdx.x == 0 && g_k1_trace && (n) < 64) {                                \
@@ -55,11 +59,12 @@ namespace halo {
 namespace {
 
 constexpr int kThreads = 384;  // 12 warps: 3 per SMSP (<= 168 registers per thread)
-constexpr int kSoftmaxThreads = 256;
-constexpr int kStagesKV = 3;
+constexpr int kSubRows = 128;  // rows per sub-tile (UMMA M)
+constexpr int kRegsSoftmax = 208, kRegsOther = 88;  // 8 x 208 + 4 x 88 warps = 12 x 168
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 between rescales
+static_assert(kK1Rows == 2 * kSubRows, "K1 tile = two UMMA M=128 sub-tiles");
 
 struct PrefixArgs {
     PlanDev p;
@@ -71,42 +76,44 @@ struct PrefixArgs {
 
 template <int D>
 struct L1 {
+    static constexpr int SK = D == 128 ? 3 : 4;    // K ring stages
+    static constexpr int SV = D == 128 ? 2 : 4;    // V ring stages
     static constexpr int ATOMS = D / 64;           // 128-B swizzle atoms along d
     static constexpr int ATOM_BYTES = 128 * 128;   // 128 rows x 128 B
-    static constexpr int Q_BYTES = 128 * D * 2;
+    static constexpr int Q_BYTES = kSubRows * D * 2;   // one sub-tile
     static constexpr int KV_BYTES = kK1Tok * D * 2;
-    static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + Q_BYTES;
-    static constexpr int OFF_V = OFF_K + kStagesKV * KV_BYTES;
-    static constexpr int OFF_BAR = OFF_V + kStagesKV * KV_BYTES;
-    static constexpr int NBAR = 24;
+    static constexpr int OFF_Q = 0;                      // Q_A | Q_B
+    static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+    static constexpr int OFF_V = OFF_K + SK * KV_BYTES;
+    static constexpr int OFF_BAR = OFF_V + SV * KV_BYTES;
+    static constexpr int NBAR = 32;
     static constexpr int OFF_BLK = OFF_BAR + NBAR * 8 + 16;       // block ids of the tile range
-    static constexpr int MAX_BLK = kK1MaxTileTok / kBlockTok;    // block ids per CTA range
-    static constexpr int OFF_X = OFF_BLK + MAX_BLK * 4;            // [2 tiles][2 halves][128] max
-    static constexpr int SMEM = OFF_X + 2 * 2 * 128 * 4;            // base must be 1024-aligned
-    static constexpr int O_STRIDE = D * 4;                       // epilogue staging row bytes
-    static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256, TMEM_P = 384;
+    static constexpr int MAX_BLK = kK1MaxTileTok / kBlockTok;
+    static constexpr int SMEM = OFF_BLK + MAX_BLK * 4;              // base must be 1024-aligned
+    static constexpr int O_STRIDE = D * 4;                          // epilogue staging row bytes
+    static __host__ __device__ constexpr uint32_t tmem_s(int x) { return x ? 128u : 0u; }
+    static __host__ __device__ constexpr uint32_t tmem_o(int x) { return x ? 384u : 256u; }
+    static_assert(SK * KV_BYTES >= kSubRows * O_STRIDE && SV * KV_BYTES >= kSubRows * O_STRIDE,
+                  "epilogue staging reuses the K ring (A) and the V ring (B)");
+    static_assert(SMEM <= 227 * 1024, "K1 shared memory exceeds the 227 KB per-CTA limit");
 };
-
-static_assert(L1<128>::SMEM <= 227 * 1024, "K1 shared memory exceeds the 227 KB per-CTA limit");
 
 enum Bar {
-    Q_FULL = 0,
-    K_FULL = 1, K_EMPTY = 4, V_FULL = 7, V_EMPTY = 10, V_CONV = 13,  // x kStagesKV
-    S_FULL = 16, S_FREE = 18, P_FULL = 20, PV_DONE = 22              // x 2
+    Q_FULL = 0,                                  // x2 (sub-tile)
+    S_FULL = 2, P_FULL = 4, PV_DONE = 6,         // x2
+    K_FULL = 8, K_EMPTY = 12,                    // x SK (<= 4)
+    V_FULL = 16, V_EMPTY = 20, V_CONV = 24,      // x SV (<= 4)
+    EXP_DONE = 28                                // x2: sub-tile x finished its exp pass
+
 };
 
-// Precision of the P operand of O += P.V (reading R8):
-//   kPBf16   bf16 P, bf16 V (fails the 2e-3 bar on sharp score distributions)
-//   kPF16    fp16 P, V converted bf16 -> fp16 in shared memory (default)
-enum PMode { kPBf16 = 0, kPF16 = 2 };
-
-template <int D, int PM>
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                    const __grid_constant__ CUtensorMap tmk8, const __grid_constant__ CUtensorMap tmv8,
                    const PrefixArgs a) {
     using C = L1<D>;
+    constexpr int SK = C::SK, SV = C::SV;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 128-B swizzle atoms need a 1024-B aligned base (the dynamic window starts aligned)
     if (ptx::smem_u32(smem_raw) & 1023) __trap();
@@ -117,22 +124,25 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     if (threadIdx.x == 0) K1_TRACE(9, 0);
     const PrefixTile T = a.p.tiles[blockIdx.x];
     const int NT = (T.tok_end - T.tok_begin + kK1Tok - 1) / kK1Tok;
+    const bool hasB = T.nrows > kSubRows;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        ptx::mbar_init(&bar[Q_FULL], kSoftmaxThreads);
-        for (int s = 0; s < kStagesKV; ++s) {
+        for (int x = 0; x < 2; ++x) {
+            ptx::mbar_init(&bar[Q_FULL + x], kSubRows);
+            ptx::mbar_init(&bar[S_FULL + x], 1);
+            ptx::mbar_init(&bar[P_FULL + x], kSubRows);
+            ptx::mbar_init(&bar[PV_DONE + x], 1);
+            ptx::mbar_init(&bar[EXP_DONE + x], kSubRows);
+        }
+        for (int s = 0; s < SK; ++s) {
             ptx::mbar_init(&bar[K_FULL + s], 1);
             ptx::mbar_init(&bar[K_EMPTY + s], 1);
+        }
+        for (int s = 0; s < SV; ++s) {
             ptx::mbar_init(&bar[V_FULL + s], 1);
             ptx::mbar_init(&bar[V_EMPTY + s], 1);
             ptx::mbar_init(&bar[V_CONV + s], 64);
-        }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&bar[S_FULL + b], 1);
-            ptx::mbar_init(&bar[S_FREE + b], kSoftmaxThreads);
-            ptx::mbar_init(&bar[P_FULL + b], kSoftmaxThreads);
-            ptx::mbar_init(&bar[PV_DONE + b], 1);
         }
         ptx::fence_barrier_init();
     }
@@ -142,9 +152,13 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // register split (setmaxnreg, per warpgroup): the softmax warpgroups hold a full
+    // 128-column score row per thread; the producer / MMA / converter warpgroup gives back
+#define HALO_REGS_DEC() asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther))
+#define HALO_REGS_INC() asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax))
     if (warp == 8) {
+        HALO_REGS_DEC();
         // ===================== TMA producer: K and V rings =====================
-        // block ids of [tok_begin, tok_end) -> smem, all lanes, independent loads
         int32_t *blocks = reinterpret_cast<int32_t *>(sm + C::OFF_BLK);
         const int blk_first = T.tok_begin / kBlockTok;
         const int nblk = (T.tok_end + kBlockTok - 1) / kBlockTok - blk_first;
@@ -182,245 +196,256 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             int nk = 0, nv = 0;
             while (nk < NT || nv < NT) {
                 const int before = nk + nv;
-                if (nk < NT && (nk < kStagesKV ||
-                                ptx::mbar_test(&bar[K_EMPTY + nk % kStagesKV], ((nk / kStagesKV) & 1) ^ 1))) {
-                    const int st = nk % kStagesKV;
-                    issue(&tmk, &tmk8, sm + C::OFF_K + st * C::KV_BYTES, &bar[K_FULL + st], nk);
+                if (nk < NT && (nk < SK || ptx::mbar_test(&bar[K_EMPTY + nk % SK], ((nk / SK) & 1) ^ 1))) {
+                    issue(&tmk, &tmk8, sm + C::OFF_K + (nk % SK) * C::KV_BYTES, &bar[K_FULL + nk % SK], nk);
                     K1_TRACE(0, nk);
                     ++nk;
                 }
                 if (nv < NT && nv <= nk &&
-                    (nv < kStagesKV ||
-                     ptx::mbar_test(&bar[V_EMPTY + nv % kStagesKV], ((nv / kStagesKV) & 1) ^ 1))) {
-                    const int st = nv % kStagesKV;
-                    issue(&tmv, &tmv8, sm + C::OFF_V + st * C::KV_BYTES, &bar[V_FULL + st], nv);
+                    (nv < SV || ptx::mbar_test(&bar[V_EMPTY + nv % SV], ((nv / SV) & 1) ^ 1))) {
+                    issue(&tmv, &tmv8, sm + C::OFF_V + (nv % SV) * C::KV_BYTES, &bar[V_FULL + nv % SV], nv);
                     K1_TRACE(1, nv);
                     ++nv;
                 }
-                if (nk + nv == before) __nanosleep(64);
+                if (nk + nv == before) __nanosleep(32);
             }
         }
     } else if (warp == 9) {
+        HALO_REGS_DEC();
         // ===================== MMA issuer (single thread) =====================
         if (lane == 0) {
             constexpr uint32_t idS = ptx::idesc_bf16(128, kK1Tok, false, false);
-            constexpr uint32_t fmtPV = PM == kPBf16 ? 1u : 0u;
-            constexpr uint32_t idO = ptx::idesc_f16(128, D, fmtPV, fmtPV, false, true);
-            const uint32_t q_base = ptx::smem_u32(sm + C::OFF_Q);
-            ptx::mbar_wait(&bar[Q_FULL], 0);
+            constexpr uint32_t idO = ptx::idesc_f16(128, D, 0u, 0u, false, true);
+            const int nsub = hasB ? 2 : 1;
+            for (int x = 0; x < nsub; ++x) ptx::mbar_wait(&bar[Q_FULL + x], 0);
             ptx::tc_fence_after();
             for (int n = 0; n <= NT; ++n) {
+                const int m = n - 1, vst = (m + SV) % SV, kst = n % SK;
                 if (n < NT) {
-                    const int st = n % kStagesKV, b = n & 1;
-                    ptx::mbar_wait(&bar[K_FULL + st], (n / kStagesKV) & 1);
-                    if (n >= 2) ptx::mbar_wait(&bar[S_FREE + b], ((n >> 1) & 1) ^ 1);
+                    ptx::mbar_wait(&bar[K_FULL + kst], (n / SK) & 1);
                     K1_TRACE(2, n);
-                    ptx::tc_fence_after();
-                    const uint32_t k_base = ptx::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off = (kk / 4) * C::ATOM_BYTES + (kk % 4) * 32;
-                        ptx::mma_bf16_ss(tmem + (b ? C::TMEM_S1 : C::TMEM_S0),
-                                         ptx::smem_desc_sw128(q_base + off, 16, 1024),
-                                         ptx::smem_desc_sw128(k_base + off, 16, 1024), idS,
-                                         kk > 0);
-                    }
-                    ptx::mma_commit(&bar[S_FULL + b]);
-                    ptx::mma_commit(&bar[K_EMPTY + st]);
                 }
                 if (n >= 1) {
-                    const int m = n - 1, st = m % kStagesKV, b = m & 1;
-                    if (PM == kPF16) ptx::mbar_wait(&bar[V_CONV + st], (m / kStagesKV) & 1);
-                    else ptx::mbar_wait(&bar[V_FULL + st], (m / kStagesKV) & 1);
-                    ptx::mbar_wait(&bar[P_FULL + b], (m >> 1) & 1);
-                    K1_TRACE(3, m);
-                    ptx::tc_fence_after();
-                    const uint32_t v_base = ptx::smem_u32(sm + C::OFF_V + st * C::KV_BYTES);
+                    ptx::mbar_wait(&bar[V_CONV + vst], (m / SV) & 1);
+                    K1_TRACE(12, m);
+                }
+                for (int x = 0; x < nsub; ++x) {
+                    if (n >= 1) {  // PV_x(m): A = P_x from TMEM (8 packed columns per 16 tokens)
+                        ptx::mbar_wait(&bar[P_FULL + x], m & 1);
+                        K1_TRACE(3 + 12 * x, m);
+                        ptx::tc_fence_after();
+                        const uint32_t v_base = ptx::smem_u32(sm + C::OFF_V + vst * C::KV_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < kK1Tok / 16; ++kk) {
-                        // A = P from TMEM: 16 tokens = 8 packed 32-bit columns per K-step.
-                        // B = V, MN-major: 64-wide d chunks LBO = 128 rows x 128 B apart,
-                        // 8-token row groups SBO = 1024 B apart; 16 tokens per step.
-                        ptx::mma_f16_ts(tmem + C::TMEM_O, tmem + C::TMEM_P + b * 64 + kk * 8,
-                                        ptx::smem_desc_sw128(v_base + kk * 16 * 128, C::ATOM_BYTES, 1024),
-                                        idO, (m > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < kK1Tok / 16; ++kk)
+                            // B = V, MN-major: 64-wide d chunks LBO = 128 rows x 128 B apart,
+                            // 8-token row groups SBO = 1024 B apart; 16 tokens per step.
+                            ptx::mma_f16_ts(tmem + C::tmem_o(x), tmem + C::tmem_s(x) + kk * 8,
+                                            ptx::smem_desc_sw128(v_base + kk * 16 * 128, C::ATOM_BYTES, 1024),
+                                            idO, (m > 0 || kk > 0) ? 1u : 0u);
+                        ptx::mma_commit(&bar[PV_DONE + x]);
+                        if (x == nsub - 1) ptx::mma_commit(&bar[V_EMPTY + vst]);
                     }
-                    ptx::mma_commit(&bar[V_EMPTY + st]);
-                    ptx::mma_commit(&bar[PV_DONE + b]);
+                    if (n < NT) {  // QK_x(n) -> S_x (overwrites P_x(m): PV_x(m) was issued first)
+                        const uint32_t q_base = ptx::smem_u32(sm + C::OFF_Q + x * C::Q_BYTES);
+                        const uint32_t k_base = ptx::smem_u32(sm + C::OFF_K + kst * C::KV_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t off = (kk / 4) * C::ATOM_BYTES + (kk % 4) * 32;
+                            ptx::mma_bf16_ss(tmem + C::tmem_s(x), ptx::smem_desc_sw128(q_base + off, 16, 1024),
+                                             ptx::smem_desc_sw128(k_base + off, 16, 1024), idS, kk > 0);
+                        }
+                        ptx::mma_commit(&bar[S_FULL + x]);
+                        if (x == nsub - 1) ptx::mma_commit(&bar[K_EMPTY + kst]);
+                    }
                 }
             }
         }
     } else if (warp >= 10) {
+        HALO_REGS_DEC();
         // ===================== V converters: bf16 -> fp16 in place =====================
-        if (PM == kPF16) {
-            const int t = threadIdx.x - 320;  // 0..63
-            for (int n = 0; n < NT; ++n) {
-                const int st = n % kStagesKV;
-                ptx::mbar_wait(&bar[V_FULL + st], (n / kStagesKV) & 1);
-                if (t == 0) K1_TRACE(4, n);
-                uint4 *vs = reinterpret_cast<uint4 *>(sm + C::OFF_V + st * C::KV_BYTES);
+        const int t = threadIdx.x - 320;  // 0..63
+        for (int n = 0; n < NT; ++n) {
+            const int st = n % SV;
+            ptx::mbar_wait(&bar[V_FULL + st], (n / SV) & 1);
+            if (t == 0) K1_TRACE(4, n);
+            uint4 *vs = reinterpret_cast<uint4 *>(sm + C::OFF_V + st * C::KV_BYTES);
 #pragma unroll 4
-                for (int c = t; c < C::KV_BYTES / 16; c += 64) {
-                    uint4 w = vs[c];
-                    float2 f;
-                    f = ptx::bf2_to_f2(w.x); w.x = ptx::f2_to_h2(f.x, f.y);
-                    f = ptx::bf2_to_f2(w.y); w.y = ptx::f2_to_h2(f.x, f.y);
-                    f = ptx::bf2_to_f2(w.z); w.z = ptx::f2_to_h2(f.x, f.y);
-                    f = ptx::bf2_to_f2(w.w); w.w = ptx::f2_to_h2(f.x, f.y);
-                    vs[c] = w;
-                }
-                ptx::fence_proxy_async_smem();
-                if (t == 0) K1_TRACE(5, n);
-                ptx::mbar_arrive(&bar[V_CONV + st]);
+            for (int c = t; c < C::KV_BYTES / 16; c += 64) {
+                uint4 w = vs[c];
+                float2 f;
+                f = ptx::bf2_to_f2(w.x); w.x = ptx::f2_to_h2(f.x, f.y);
+                f = ptx::bf2_to_f2(w.y); w.y = ptx::f2_to_h2(f.x, f.y);
+                f = ptx::bf2_to_f2(w.z); w.z = ptx::f2_to_h2(f.x, f.y);
+                f = ptx::bf2_to_f2(w.w); w.w = ptx::f2_to_h2(f.x, f.y);
+                vs[c] = w;
             }
+            ptx::fence_proxy_async_smem();
+            if (t == 0) K1_TRACE(5, n);
+            ptx::mbar_arrive(&bar[V_CONV + st]);
         }
     } else {
-        // ===================== softmax warpgroups (warps 0..7) =====================
-        constexpr int HC = kK1Tok / 2;          // columns per half
-        const int h = warp >> 2;                // column half
+        HALO_REGS_INC();
+        // ===================== softmax warpgroups: A = warps 0-3, B = warps 4-7 =====================
+        const int x = warp >> 2;                // sub-tile
+        if (x == 1 && !hasB) goto done;
+        {
         const int wq = warp & 3;
-        const int r = wq * 32 + lane;           // tile row == TMEM lane
-        const int st_id = threadIdx.x;          // 0..255
+        const int r = wq * 32 + lane;           // sub-tile row == TMEM lane
+        const int trow = x * kSubRows + r;      // tile row
         const uint32_t lane_addr = tmem + ((uint32_t)(32 * wq) << 16);
-        const bool valid_row = r < T.nrows;
+        const bool valid_row = trow < T.nrows;
         const int g = a.g;
-        const int req = valid_row ? a.p.req_order[T.req_off + r / g] : 0;
-        const int head = T.kv_head * g + r % g;
-        float *xmax = reinterpret_cast<float *>(sm + C::OFF_X);  // [2][2][128]
-        // Q row -> smem, K-major SW128 (16-B chunk c of row r lands at chunk c ^ (r & 7));
-        // each half loads half of the row's chunks
+        const int req = valid_row ? a.p.req_order[T.req_off + trow / g] : 0;
+        const int head = T.kv_head * g + trow % g;
+        // Q row -> smem, K-major SW128 (16-B chunk c of row r lands at chunk c ^ (r & 7))
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.q + ((int64_t)req * a.hq + head) * D);
-            uint8_t *qs = sm + C::OFF_Q;
+            uint8_t *qs = sm + C::OFF_Q + x * C::Q_BYTES;
 #pragma unroll
-            for (int cc0 = 0; cc0 < D / 16; ++cc0) {
-                const int c = h * (D / 16) + cc0;
+            for (int c = 0; c < D / 8; ++c) {
                 const uint4 v = valid_row ? src[c] : make_uint4(0, 0, 0, 0);
                 const int at = c / 8, cc = c % 8;
                 *reinterpret_cast<uint4 *>(qs + at * C::ATOM_BYTES + r * 128 + ((cc ^ (r & 7)) * 16)) = v;
             }
             ptx::fence_proxy_async_smem();
-            if (st_id == 0) K1_TRACE(9, 2);
-            ptx::mbar_arrive(&bar[Q_FULL]);
+            if (threadIdx.x == 0) K1_TRACE(9, 2);
+            ptx::mbar_arrive(&bar[Q_FULL + x]);
         }
-        float m_ref = -INFINITY, l = 0.f;
+        const uint32_t s_addr = lane_addr + C::tmem_s(x);
+        const uint32_t o_addr = lane_addr + C::tmem_o(x);
         const float c2 = a.qscale;
+        float m_ref = -INFINITY, l = 0.f;
         for (int n = 0; n < NT; ++n) {
-            const int b = n & 1;
-            ptx::mbar_wait(&bar[S_FULL + b], (n >> 1) & 1);
-            if (st_id == 0) K1_TRACE(6, n);
+            ptx::mbar_wait(&bar[S_FULL + x], n & 1);
+            if (threadIdx.x == 0) K1_TRACE(6, n);
+            if (threadIdx.x == 128) K1_TRACE(14, n);
             ptx::tc_fence_after();
-            const uint32_t s_addr = lane_addr + (b ? C::TMEM_S1 : C::TMEM_S0) + h * HC;
-            const int valid = min(kK1Tok, T.tok_end - (T.tok_begin + n * kK1Tok)) - h * HC;
-            uint32_t sr[HC];
+            const int valid = min(kK1Tok, T.tok_end - (T.tok_begin + n * kK1Tok));
+            // the whole 128-column score row in registers: one TMEM round trip per n-tile
+            uint32_t sr[kK1Tok];
             HALO_TMEM_LD32(s_addr, sr);
             HALO_TMEM_LD32(s_addr + 32, (sr + 32));
-            ptx::tmem_wait_ld();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&bar[S_FREE + b]);
-            if (valid < HC) {  // only in a node's last tile: columns past the end -> -inf
+            HALO_TMEM_LD32(s_addr + 64, (sr + 64));
+            HALO_TMEM_LD32(s_addr + 96, (sr + 96));
+            HALO_TMEM_WAIT_LD_REGS32(sr);
+            HALO_TMEM_WAIT_LD_REGS32((sr + 32));
+            HALO_TMEM_WAIT_LD_REGS32((sr + 64));
+            HALO_TMEM_WAIT_LD_REGS32((sr + 96));
+            if (valid < kK1Tok) {  // only in a node's last n-tile: columns past the end -> -inf
 #pragma unroll
-                for (int i = 0; i < HC; ++i)
+                for (int i = 0; i < kK1Tok; ++i)
                     if (i >= valid) sr[i] = __float_as_uint(-INFINITY);
             }
-            float mxv[8];
+            float mxv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) mxv[i] = __uint_as_float(sr[i]);
+            for (int i = 0; i < kK1Tok; i += 2)
+                mxv[(i >> 1) & 3] = fmaxf(mxv[(i >> 1) & 3], fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+            const float mx = fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3]));
+            if (threadIdx.x == 0) K1_TRACE(10, n);
+            // lazy reference max: move it (and rescale O) only when a row's max grew by > 2^8
+            const bool grow = mx * c2 > m_ref + kRescaleThreshold;
+            if (__any_sync(0xffffffffu, grow)) {
+                const float m_new = grow ? mx * c2 : m_ref;
+                const float alpha = ptx::ex2(m_ref - m_new);  // 0 on a row's first tile
+                if (n >= 1) {
+                    ptx::mbar_wait(&bar[PV_DONE + x], (n - 1) & 1);  // O stable
+                    ptx::tc_fence_after();
+#pragma unroll 1
+                    for (int k = 0; k < D / 32; ++k) {
+                        uint32_t ov[32];
+                        HALO_TMEM_LD32(o_addr + 32 * k, ov);
+                        HALO_TMEM_WAIT_LD_REGS32(ov);
 #pragma unroll
-            for (int i = 8; i < HC; ++i) mxv[i & 7] = fmaxf(mxv[i & 7], __uint_as_float(sr[i]));
-            float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                             fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
-            // exchange the half-row maxima (double-buffered by tile parity)
-            xmax[(b * 2 + h) * 128 + r] = mx;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            mx = fmaxf(mx, xmax[(b * 2 + (h ^ 1)) * 128 + r]);
-            if (st_id == 0) K1_TRACE(7, n);
-            const float mx2 = mx * c2;
-            const bool grow = mx2 > m_ref + kRescaleThreshold;
-            const float m_use = grow ? mx2 : m_ref;
-            const float alpha = ptx::ex2(m_ref - m_use);  // 0 on the first tile
-            if (n >= 2) ptx::mbar_wait(&bar[PV_DONE + b], ((n >> 1) - 1) & 1);  // P[b] consumed
-            if (n >= 1 && __any_sync(0xffffffffu, grow)) {
-                ptx::mbar_wait(&bar[PV_DONE + (b ^ 1)], ((n - 1) >> 1) & 1);  // O stable
-                ptx::tc_fence_after();
-#pragma unroll
-                for (int k = 0; k < D / 64; ++k) {
-                    uint32_t ov[32];
-                    const uint32_t oa = lane_addr + C::TMEM_O + h * (D / 2) + 32 * k;
-                    HALO_TMEM_LD32(oa, ov);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-                    HALO_TMEM_ST32(oa, ov);
+                        for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                        HALO_TMEM_ST32(o_addr + 32 * k, ov);
+                    }
                 }
+                l *= alpha;
+                m_ref = m_new;
             }
-            m_ref = m_use;
-            ptx::tc_fence_after();
-            if (st_id == 0) K1_TRACE(10, n);
-            // p = 2^(s*c - m) (masked scores give 0), packed 16-bit pairs -> TMEM P[b]
-            const float2 c2v = make_float2(c2, c2), nm = make_float2(-m_use, -m_use);
-            float2 psv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            // p = 2^(s*c - m_ref) -> fp16 pairs over the consumed S columns.  MUFU ping-pong:
+            // A's exp pass of tile n follows B's of tile n-1 and B's follows A's of tile n, so
+            // one warpgroup's exponentials overlap the other's MMAs
+            if (hasB) {
+                if (x == 1) ptx::mbar_wait(&bar[EXP_DONE + 0], n & 1);
+                else if (n >= 1) ptx::mbar_wait(&bar[EXP_DONE + 1], (n - 1) & 1);
+            }
+            if (threadIdx.x == 0) K1_TRACE(7, n);
+            const float2 c2v = make_float2(c2, c2), nm = make_float2(-m_ref, -m_ref);
+            float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                             make_float2(0.f, 0.f)};
 #pragma unroll
-            for (int k = 0; k < HC / 32; ++k) {
+            for (int k = 0; k < kK1Tok / 32; ++k) {
+                // 32 independent exponentials back to back (one MUFU warp instruction per 8
+                // cycles), four accumulators, pack, then P chunk k -> columns [16k, 16k+16)
+                float2 e[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    e[i] = ptx::ffma2(make_float2(__uint_as_float(sr[32 * k + 2 * i]), __uint_as_float(sr[32 * k + 2 * i + 1])), c2v, nm);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    e[i].x = ptx::ex2(e[i].x);
+                    e[i].y = ptx::ex2(e[i].y);
+                }
                 uint32_t pk[16];
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const int col = 32 * k + i;
-                    float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[col]), __uint_as_float(sr[col + 1])), c2v, nm);
-                    x.x = ptx::ex2(x.x);
-                    x.y = ptx::ex2(x.y);
-                    psv[(i >> 1) & 1] = ptx::fadd2(psv[(i >> 1) & 1], x);
-                    pk[i / 2] = PM == kPBf16 ? ptx::f2_to_bf2(x.x, x.y) : ptx::f2_to_h2(x.x, x.y);
+                for (int i = 0; i < 16; ++i) {
+                    acc[i & 3] = ptx::fadd2(acc[i & 3], e[i]);
+                    pk[i] = ptx::f2_to_h2(e[i].x, e[i].y);
                 }
-                HALO_TMEM_ST16(lane_addr + C::TMEM_P + b * 64 + h * (HC / 2) + 16 * k, pk);
+                HALO_TMEM_ST16(s_addr + 16 * k, pk);
             }
-            if (st_id == 0) K1_TRACE(11, n);
-            l = l * alpha + ((psv[0].x + psv[0].y) + (psv[1].x + psv[1].y));
+            const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
+            l += (a01.x + a01.y) + (a23.x + a23.y);
+            if (hasB) ptx::mbar_arrive(&bar[EXP_DONE + x]);
+            if (threadIdx.x == 0) K1_TRACE(11, n);
+            if (threadIdx.x == 128) K1_TRACE(13, n);
             ptx::tmem_wait_st();
-            if (st_id == 0) K1_TRACE(8, n);
+            if (threadIdx.x == 0) K1_TRACE(8, n);
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&bar[P_FULL + b]);
+            ptx::mbar_arrive(&bar[P_FULL + x]);
         }
         // ---- epilogue: O / l -> normalised partial, lse ----
-        ptx::mbar_wait(&bar[PV_DONE + ((NT - 1) & 1)], ((NT - 1) >> 1) & 1);
+        ptx::mbar_wait(&bar[PV_DONE + x], (NT - 1) & 1);
         ptx::tc_fence_after();
-        xmax[h * 128 + r] = l;  // row sums of the two halves (same reference max)
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        l += xmax[(h ^ 1) * 128 + r];
         const float inv = 1.f / l;
-        // row r, this half's d columns -> smem staging (16-B chunks XOR-swizzled by row)
-        uint8_t *stage = sm + C::OFF_K;  // K ring is free once the last PV completed
+        // staging: sub-tile A in the K ring, B in the V ring (both idle once PV_x(NT-1) is done);
+        // row r's 16-B chunks XOR-swizzled by row
+        uint8_t *stage = sm + (x == 0 ? C::OFF_K : C::OFF_V);
 #pragma unroll
-        for (int k = 0; k < D / 64; ++k) {
+        for (int k = 0; k < D / 32; ++k) {
             uint32_t ov[32];
-            HALO_TMEM_LD32(lane_addr + C::TMEM_O + h * (D / 2) + 32 * k, ov);
+            HALO_TMEM_LD32(o_addr + 32 * k, ov);
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int c = h * (D / 8) + k * 8 + i;
+                const int c = k * 8 + i;
                 *reinterpret_cast<float4 *>(stage + r * C::O_STRIDE + ((c ^ (r & 7)) * 16)) =
                     make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
                                 __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
             }
         }
         const int64_t row = ((int64_t)T.slot * a.p.nreq + req) * a.hq + head;
-        int64_t *row_off = reinterpret_cast<int64_t *>(sm + C::OFF_V);  // V ring is free too
-        if (h == 0) row_off[r] = valid_row ? row * D : -1;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        int64_t *row_off = reinterpret_cast<int64_t *>(sm + C::OFF_Q + x * C::Q_BYTES);  // Q_x is dead
+        row_off[r] = valid_row ? row * D : -1;
+        if (x == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+        else asm volatile("bar.sync 2, 128;" ::: "memory");
         // each warp writes whole rows: lane = 16-B chunk (d=128: 32 chunks = 512 B per row)
         constexpr int CPR = D / 4;
         constexpr int RPI = 32 / CPR;  // rows per warp instruction
-        for (int rr = warp * RPI; rr < 128; rr += 8 * RPI) {
+        for (int rr = wq * RPI; rr < kSubRows; rr += 4 * RPI) {
             const int row_i = rr + lane / CPR, c = lane % CPR;
             const int64_t off = row_off[row_i];
             if (off >= 0)
                 reinterpret_cast<float4 *>(a.p.part_o + off)[c] =
                     *reinterpret_cast<const float4 *>(stage + row_i * C::O_STRIDE + ((c ^ (row_i & 7)) * 16));
         }
-        if (valid_row && h == 0) a.p.part_lse[row] = (m_ref + __log2f(l)) * kLn2;
-        if (st_id == 0) K1_TRACE(9, 1);
+        if (valid_row) a.p.part_lse[row] = (m_ref + __log2f(l)) * kLn2;
+        if (threadIdx.x == 0) K1_TRACE(9, 1);
         ptx::tc_fence_before();
+        }
     }
+done:
     __syncthreads();
     if (warp == 9) {
         ptx::tc_fence_after();
@@ -428,10 +453,10 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     }
 }
 
-template <int D, int PM>
+template <int D>
 cudaError_t launch_t(const CUtensorMap *tmk, const CUtensorMap *tmv, const CUtensorMap *tmk8,
                      const CUtensorMap *tmv8, const PrefixArgs &a, cudaStream_t s) {
-    auto kern = prefix_attn_kernel<D, PM>;
+    auto kern = prefix_attn_kernel<D>;
     int dev = 0;
     cudaGetDevice(&dev);
     static bool configured[64] = {};
@@ -459,15 +484,8 @@ cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tma
     a.g = g.hq / g.hkv;
     a.layer_blk = (int64_t)layer * g.cap;
     a.qscale = scale * kLog2e;
-    static const int pmode = [] {
-        const char *e = getenv("HALO_K1_PMODE");
-        return e ? atoi(e) : (int)kPF16;
-    }();
-#define HALO_K1_CASE(DD, PMM) \
-    if (g.d == DD && pmode == PMM) return launch_t<DD, PMM>(tmap_k, tmap_v, tmap_k8, tmap_v8, a, s);
-    HALO_K1_CASE(128, kPBf16) HALO_K1_CASE(128, kPF16)
-    HALO_K1_CASE(64, kPBf16) HALO_K1_CASE(64, kPF16)
-#undef HALO_K1_CASE
+    if (g.d == 128) return launch_t<128>(tmap_k, tmap_v, tmap_k8, tmap_v8, a, s);
+    if (g.d == 64) return launch_t<64>(tmap_k, tmap_v, tmap_k8, tmap_v8, a, s);
     return cudaErrorInvalidValue;
 }
 

@@ -139,7 +139,7 @@ def test_plan_dfs_ranges_are_contiguous_and_tiles_cover_every_row_token_once():
         g = wl.g
         covered = {}
         for (req_off, nrows, head, t0, t1, blk_off, slot, node) in tiles:
-            assert 0 < nrows <= 128 and t0 % 128 == 0 and t1 > t0
+            assert 0 < nrows <= 256 and t0 % 128 == 0 and t1 > t0
             for row in range(nrows):
                 r = int(order[req_off + row // g])
                 for t in sorted({int(t0), int(t1) - 1}):

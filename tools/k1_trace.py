@@ -19,7 +19,8 @@ from paper_2509_02121_b200.loader import append_step, load  # noqa: E402
 from synth import make_config  # noqa: E402
 
 EV = ["K issued", "V issued", "QK issue", "PV issue", "V full(conv)", "V conv done",
-      "S full(smax)", "pass1 done", "P stored", None, "waits done", "exp done"]
+      "S full(smax)", "pass start", "P stored", None, "pass1 done", "exp done",
+      "MMA Vconv ok", "B exp done", "B S full", "PV_B issue"]
 
 
 def main():
@@ -30,7 +31,7 @@ def main():
     plan = ld.pool.plan(ld.req_ids)
     q = wl.q(0, "cuda:0")
     out = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda:0")
-    buf = torch.zeros(12 * 64, dtype=torch.int64, device="cuda:0")
+    buf = torch.zeros(16 * 64, dtype=torch.int64, device="cuda:0")
     lib = halo.load_library()
     lib.halo_debug_k1_trace.argtypes = [ctypes.c_void_p]
     for it in range(3):
@@ -38,7 +39,7 @@ def main():
         lib.halo_debug_k1_trace(ctypes.c_void_p(buf.data_ptr()))
         plan.run_stages(0, 1, q[0], out)
         torch.cuda.synchronize()
-    t = buf.view(12, 64).cpu()
+    t = buf.view(16, 64).cpu()
     t0 = int(t[9, 0])
     print("tile0 info:", plan.export("tiles")[0].tolist())
     print(f"q loaded {(int(t[9,2])-t0)/1e3:.2f} us, epilogue done {(int(t[9,1])-t0)/1e3:.2f} us")

@@ -361,10 +361,8 @@ def main():
         e2e_steps = min(args.steps, 30)
 
         def e2e_step():
-            pool.truncate(reqs, ones)
-            pool.append(reqs, ones, nk_h, nv_h)
-            pool.plan(reqs, popt, reuse=plan)
-            plan.run_layers(L, q_h, out_h)
+            pool.truncate(reqs, ones)             # stationary batch (host bookkeeping only)
+            pool.decode_step(reqs, nk_h, nv_h, q_h, out_h, options=popt, reuse=plan)
         for _ in range(3):
             e2e_step()
         torch.cuda.synchronize()
@@ -375,16 +373,15 @@ def main():
             e2e_step()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([dt], device=f"cuda:{dev}")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = tt.item()
+        from paper_2509_02121_b200.sharding import max_over_ranks
+        dt = max_over_ranks([dt], dist if world > 1 else None, f"cuda:{dev}")[0]
         h2d = nk_h.numel() * 2 * 2 + q_h.numel() * 2
         d2h = out_h.numel() * 4
         extra["e2e"] = {"value": R * L * world * e2e_steps / dt, "unit": UNIT,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                        "steps": e2e_steps, "how": "halo_suffix_append + halo_decode_plan + "
-                        "halo_decode_layers with pinned host buffers; wall clock after sync"}
+                        "steps": e2e_steps, "how": "halo_decode_step (append one token per request + "
+                        "plan + all layers; per-layer H2D/D2H on library copy streams overlapped "
+                        "with the kernels) with pinned host buffers; wall clock after sync"}
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
         extra["migration"] = measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist)

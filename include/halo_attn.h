@@ -167,6 +167,19 @@ halo_status halo_decode_plan(halo_pool pool, int32_t nreq, const int64_t *reqs,
  * Graph-capturable. */
 halo_status halo_decode_run(halo_plan plan, int32_t layer, const void *q, float *out,
                             float *lse, float scale, void *stream);
+/* One decode step of the batch, the call a serving loop makes (PAPER.md:341 decode batch;
+ * append-then-attend, R4): append ONE token per request (k_new, v_new: bf16
+ * [num_layers][nreq][num_kv_heads][head_dim]), (re)plan into *inout (NULL: a new plan, as
+ * halo_decode_plan), then attention of every layer (q: bf16 [num_layers][nreq][Hq][d];
+ * out: fp32 [num_layers][nreq][Hq][d]; lse nullable fp32 [num_layers][nreq][Hq]).
+ * Every buffer may be host (pinned for overlap) or device.  Pipelined per layer: the
+ * host->device copies of layer l+1 and the device->host copy of layer l-1 overlap the
+ * append + K1 + K2/K3 kernels of layer l (two library-owned copy streams, events).  All
+ * work is complete in `stream` order when the call's work on `stream` is.  Errors before
+ * any launch (ENOENT, ENOMEM, EINVAL) leave the pool unchanged. */
+halo_status halo_decode_step(halo_pool pool, int32_t nreq, const int64_t *reqs, const void *k_new,
+                             const void *v_new, const void *q, float *out, float *lse, float scale,
+                             const halo_plan_options *opt, void *stream, halo_plan *inout);
 /* Run only some stages of halo_decode_run (for per-kernel timing): stage_mask bit 0 = K1
  * (prefix partials), bit 1 = K2+K3 (suffix + merge; reads the partials K1 last wrote for
  * this plan).  halo_decode_run == stage_mask 3. */

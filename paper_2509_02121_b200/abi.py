@@ -61,6 +61,8 @@ SIGNATURES = {
     "halo_decode_run": (_i32, [_p, _i32, _p, _p, _p, _f, _p]),
     "halo_decode_run_stages": (_i32, [_p, _i32, _i32, _p, _p, _p, _f, _p]),
     "halo_decode_layers": (_i32, [_p, _i32, _p, _p, _p, _f, _p]),
+    "halo_decode_step": (_i32, [_p, _i32, _pi64, _p, _p, _p, _p, _p, _f, C.POINTER(PlanOptions), _p,
+                                C.POINTER(_p)]),
     "halo_plan_get_info": (_i32, [_p, C.POINTER(PlanInfo)]),
     "halo_plan_export": (_i32, [_p, _i32, _p, _i64, _pi64]),
     "halo_plan_destroy": (_i32, [_p]),
@@ -243,6 +245,19 @@ class Pool:
         h = C.c_void_p(reuse.handle.value if reuse is not None else None)
         _call("halo_decode_plan", self.handle, len(reqs), _i64_array(reqs),
               C.byref(options) if options is not None else None, self._s(stream), C.byref(h))
+        if reuse is not None:
+            reuse.nreq = len(reqs)
+            return reuse
+        return Plan(self, h, len(reqs))
+
+    def decode_step(self, reqs, k_new, v_new, q, out, lse=None, scale: float = 0.0,
+                    options: PlanOptions | None = None, stream=None, reuse: "Plan" = None):
+        """halo_decode_step: append one token per request, (re)plan, attend every layer,
+        with per-layer overlap of host<->device copies (host tensors should be pinned)."""
+        h = C.c_void_p(reuse.handle.value if reuse is not None else None)
+        _call("halo_decode_step", self.handle, len(reqs), _i64_array(reqs), _ptr(k_new), _ptr(v_new),
+              _ptr(q), _ptr(out), _ptr(lse), scale, C.byref(options) if options is not None else None,
+              self._s(stream), C.byref(h))
         if reuse is not None:
             reuse.nreq = len(reqs)
             return reuse

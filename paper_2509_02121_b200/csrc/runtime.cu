@@ -645,8 +645,14 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const size_t o_ent = off; off = align16(off + pl->k2_ent.size() * 4);
     const size_t o_umeta = off; off = align16(off + pl->unit_meta.size() * 4);
     const size_t total = off;
-    pl->host_buf.resize(total);
-    uint8_t *h = pl->host_buf.data();
+    uint8_t *h;
+    if (p->host_only) {
+        pl->host_buf.resize(total);
+        h = pl->host_buf.data();
+    } else {
+        h = static_cast<uint8_t *>(pl->pin_plan.acquire(total));
+        if (!h) return fail(HALO_ENOMEM, "pinned plan staging (%zu bytes)", total);
+    }
     auto put = [&](size_t o, const void *src, size_t n) { if (n) memcpy(h + o, src, n); };
     put(o_tiles, pl->tiles.data(), pl->tiles.size() * sizeof(PrefixTile));
     put(o_order, pl->req_order.data(), nreq * 4);
@@ -710,7 +716,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
         pl->counter_cap = cap;
     }
     HALO_CUDA(cudaMemsetAsync(pl->counters, 0, ((size_t)U + 2) * 4, s));
-    HALO_CUDA(cudaMemcpyAsync(pl->dbuf, h, total, cudaMemcpyHostToDevice, s));
+    HALO_CUDA(pl->pin_plan.commit(pl->dbuf, total, s));
     uint8_t *d = static_cast<uint8_t *>(pl->dbuf);
     PlanDev &dv = pl->dev;
     dv.tiles = reinterpret_cast<const PrefixTile *>(d + o_tiles);
@@ -1056,14 +1062,21 @@ halo_status halo_request_info(halo_pool p, int64_t req, int64_t *leaf, int32_t *
     return HALO_OK;
 }
 
-halo_status halo_suffix_append(halo_pool p, int32_t nreq, const int64_t *reqs, const int32_t *ntok,
-                               const void *k, const void *v, void *stream) {
-    HALO_GUARD_BEGIN
-    if (check_pool(p)) return HALO_EINVAL;
+// Host half of an append: validate (repeated ids allowed), allocate the new blocks and the
+// pool slot of every new token in input order.  Nothing is committed: `work` holds the new
+// (len, blocks) of every touched request; append_commit applies it, and on a later failure
+// unalloc_blocks(fresh) undoes the allocation.
+struct AppendWork {
+    std::vector<int32_t> slots, fresh;
+    std::unordered_map<int64_t, std::pair<int32_t, std::vector<int32_t>>> req;
+    int64_t total = 0;
+};
+
+halo_status append_prepare(halo_pool p, int32_t nreq, const int64_t *reqs, const int32_t *ntok, AppendWork &w) {
     if (nreq < 0 || (nreq > 0 && (!reqs || !ntok))) return fail(HALO_EINVAL, "bad request list");
-    // simulate (handles repeated ids), validate, count new blocks
     std::unordered_map<int64_t, std::pair<int32_t, int64_t>> sim;  // id -> (len, nblocks)
-    int64_t total = 0, new_blocks = 0;
+    int64_t new_blocks = 0;
+    w.total = 0;
     for (int i = 0; i < nreq; ++i) {
         auto it = p->requests.find(reqs[i]);
         if (it == p->requests.end()) return fail(HALO_ENOENT, "unknown request %lld", (long long)reqs[i]);
@@ -1079,56 +1092,68 @@ halo_status halo_suffix_append(halo_pool p, int32_t nreq, const int64_t *reqs, c
             f->second.second = need;
         }
         f->second.first = (int32_t)len;
-        total += ntok[i];
+        w.total += ntok[i];
     }
-    if (total == 0) return HALO_OK;
-    if (!p->host_only && (!k || !v)) return fail(HALO_EINVAL, "null k/v");
-    DeviceGuard dg(p);
-    std::vector<int32_t> fresh;
-    halo_status st = alloc_blocks(p, new_blocks, fresh);
+    if (w.total == 0) return HALO_OK;
+    halo_status st = alloc_blocks(p, new_blocks, w.fresh);
     if (st != HALO_OK) return st;
-    // slot of every new token, in input order
-    std::unordered_map<int64_t, std::pair<int32_t, std::vector<int32_t>>> work;
-    std::vector<int32_t> slots;
-    slots.reserve(total);
+    w.slots.reserve(w.total);
     size_t fi = 0;
     for (int i = 0; i < nreq; ++i) {
-        auto w = work.find(reqs[i]);
-        if (w == work.end()) {
-            const Request &r = p->requests[reqs[i]];
-            w = work.emplace(reqs[i], std::make_pair(r.len, r.blocks)).first;
+        auto r = w.req.find(reqs[i]);
+        if (r == w.req.end()) {
+            const Request &rq = p->requests[reqs[i]];
+            r = w.req.emplace(reqs[i], std::make_pair(rq.len, rq.blocks)).first;
         }
         for (int32_t t = 0; t < ntok[i]; ++t) {
-            const int32_t pos = w->second.first++;
-            if (pos % kBlockTok == 0 && pos / kBlockTok >= (int32_t)w->second.second.size())
-                w->second.second.push_back(fresh[fi++]);
-            slots.push_back(w->second.second[pos / kBlockTok] * kBlockTok + pos % kBlockTok);
+            const int32_t pos = r->second.first++;
+            if (pos % kBlockTok == 0 && pos / kBlockTok >= (int32_t)r->second.second.size())
+                r->second.second.push_back(w.fresh[fi++]);
+            w.slots.push_back(r->second.second[pos / kBlockTok] * kBlockTok + pos % kBlockTok);
         }
     }
+    return HALO_OK;
+}
+
+void append_commit(halo_pool p, AppendWork &w) {
+    for (auto &r : w.req) {
+        Request &rq = p->requests[r.first];
+        rq.len = r.second.first;
+        rq.blocks = std::move(r.second.second);
+    }
+}
+
+halo_status halo_suffix_append(halo_pool p, int32_t nreq, const int64_t *reqs, const int32_t *ntok,
+                               const void *k, const void *v, void *stream) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (nreq < 0 || (nreq > 0 && (!reqs || !ntok))) return fail(HALO_EINVAL, "bad request list");
+    for (int i = 0; i < nreq; ++i)
+        if (ntok[i] > 0 && !p->host_only && (!k || !v)) return fail(HALO_EINVAL, "null k/v");
+    DeviceGuard dg(p);
+    AppendWork w;
+    halo_status st = append_prepare(p, nreq, reqs, ntok, w);
+    if (st != HALO_OK || w.total == 0) return st;
     if (!p->host_only) {
         cudaStream_t s = (cudaStream_t)stream;
-        const size_t bytes = (size_t)p->cfg.num_layers * total * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
+        const size_t bytes = (size_t)p->cfg.num_layers * w.total * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
         Scratch ss, sk, sv;
         const void *dk = nullptr, *dvp = nullptr;
-        st = upload(slots.data(), slots.size() * 4, s, ss);
+        st = upload(w.slots.data(), w.slots.size() * 4, s, ss);
         if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
         if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
         if (st == HALO_OK) {
-            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, total, (const int32_t *)ss.ptr,
-                                              total, 0, 0, p->cfg.num_layers, p->num_sms, s);
+            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, w.total, (const int32_t *)ss.ptr,
+                                              w.total, 0, 0, p->cfg.num_layers, p->num_sms, s);
             if (e != cudaSuccess) st = fail(HALO_ECUDA, "scatter launch: %s", cudaGetErrorString(e));
         }
         if (st != HALO_OK) {
-            unalloc_blocks(p, fresh, 0);
+            unalloc_blocks(p, w.fresh, 0);
             return st;
         }
         note_stream(p, s);
     }
-    for (auto &w : work) {
-        Request &r = p->requests[w.first];
-        r.len = w.second.first;
-        r.blocks = std::move(w.second.second);
-    }
+    append_commit(p, w);
     return HALO_OK;
     HALO_GUARD_END
 }
@@ -1180,6 +1205,7 @@ halo_status halo_decode_plan(halo_pool p, int32_t nreq, const int64_t *reqs, con
             if (pl->part) cudaFree(pl->part);
             if (pl->segbuf) cudaFree(pl->segbuf);
             if (pl->counters) cudaFree(pl->counters);
+            pl->pin_plan.release();
             delete pl;
         }
         return st;
@@ -1275,6 +1301,131 @@ halo_status halo_decode_layers(halo_plan pl, int32_t nlayers, const void *q, flo
     HALO_GUARD_END
 }
 
+halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, const void *k_new,
+                             const void *v_new, const void *q, float *out, float *lse, float scale,
+                             const halo_plan_options *opt, void *stream, halo_plan *inout) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (p->host_only) return fail(HALO_EUNSUPPORTED, "compute on a host-only pool");
+    if (!inout || nreq < 1 || !reqs) return fail(HALO_EINVAL, "need nreq >= 1, reqs and a plan slot");
+    if (!k_new || !v_new || !q || !out) return fail(HALO_EINVAL, "null k/v/q/out");
+    if (*inout && (*inout)->pool != p) return fail(HALO_EINVAL, "plan belongs to another pool");
+    if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)p->cfg.head_dim);
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = p->cfg.num_layers, Hq = p->cfg.num_q_heads, Hkv = p->cfg.num_kv_heads, D = p->cfg.head_dim;
+    // 1. host bookkeeping of the append (one token per request), then the plan
+    std::vector<int32_t> ones(nreq, 1);
+    AppendWork w;
+    halo_status st = append_prepare(p, nreq, reqs, ones.data(), w);
+    if (st != HALO_OK) return st;
+    std::vector<std::pair<int64_t, std::pair<int32_t, std::vector<int32_t>>>> undo;
+    for (auto &r : w.req) undo.push_back({r.first, {p->requests[r.first].len, p->requests[r.first].blocks}});
+    append_commit(p, w);
+    auto rollback = [&]() {
+        for (auto &u : undo) {
+            Request &rq = p->requests[u.first];
+            rq.len = u.second.first;
+            rq.blocks = u.second.second;
+        }
+        unalloc_blocks(p, w.fresh, 0);
+    };
+    st = halo_decode_plan(p, nreq, reqs, opt, stream, inout);
+    if (st != HALO_OK) {
+        rollback();
+        return st;
+    }
+    halo_plan pl = *inout;
+    // 2. streams, events and staging (grown once)
+    auto grow = [&](void **buf, size_t *cap, size_t bytes) -> halo_status {
+        if (*cap >= bytes) return HALO_OK;
+        if (*buf) {
+            HALO_CUDA(cudaDeviceSynchronize());
+            cudaFree(*buf);
+            *buf = nullptr;
+        }
+        HALO_CUDA(cudaMalloc(buf, bytes));
+        *cap = bytes;
+        return HALO_OK;
+    };
+    const size_t kv_layer = (size_t)nreq * Hkv * D;     // elements of one layer's new K (or V)
+    const size_t q_layer = (size_t)nreq * Hq * D, rows = (size_t)nreq * Hq;
+    const bool kv_host = !is_device_ptr(k_new) || !is_device_ptr(v_new);
+    const bool q_host = !is_device_ptr(q), o_host = !is_device_ptr(out), l_host = lse && !is_device_ptr(lse);
+    if (!pl->h2d) {
+        HALO_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking));
+        HALO_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking));
+        HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_step, cudaEventDisableTiming));
+        HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_copied, cudaEventDisableTiming));
+    }
+    while ((int)pl->ev_in.size() < L) {
+        cudaEvent_t a, b;
+        HALO_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        HALO_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        pl->ev_in.push_back(a);
+        pl->ev_out.push_back(b);
+    }
+    if (kv_host && (st = grow(&pl->kv_stage, &pl->kv_stage_cap, 2 * kv_layer * L * 2)) != HALO_OK) return st;
+    if (q_host && (st = grow(&pl->q_stage, &pl->q_stage_cap, q_layer * L * 2)) != HALO_OK) return st;
+    if (o_host && (st = grow((void **)&pl->o_stage, &pl->o_stage_cap, q_layer * L * 4)) != HALO_OK) return st;
+    if (l_host && (st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * L * 4)) != HALO_OK) return st;
+    if ((st = grow((void **)&pl->slot_stage, &pl->slot_stage_cap, w.slots.size() * 4)) != HALO_OK) return st;
+    {
+        void *hs = pl->pin_slots.acquire(w.slots.size() * 4);
+        if (!hs) return fail(HALO_ENOMEM, "pinned slot staging");
+        memcpy(hs, w.slots.data(), w.slots.size() * 4);
+        HALO_CUDA(pl->pin_slots.commit(pl->slot_stage, w.slots.size() * 4, s));
+    }
+    // 3. per-layer pipeline: H2D (k, v, q of layer l) on the h2d stream | K5 append + K1 +
+    //    K2/K3 of layer l on `stream` | D2H (out of layer l) on the d2h stream.  The staging
+    //    buffers are reused step to step: the copy streams first wait for `stream`.
+    HALO_CUDA(cudaEventRecord(pl->ev_step, s));
+    HALO_CUDA(cudaStreamWaitEvent(pl->h2d, pl->ev_step, 0));
+    HALO_CUDA(cudaStreamWaitEvent(pl->d2h, pl->ev_step, 0));
+    uint16_t *sk = static_cast<uint16_t *>(pl->kv_stage), *sv = sk ? sk + kv_layer * L : nullptr;
+    for (int l = 0; l < L; ++l) {
+        if (kv_host) {
+            HALO_CUDA(cudaMemcpyAsync(sk + kv_layer * l, static_cast<const uint16_t *>(k_new) + kv_layer * l,
+                                      kv_layer * 2, cudaMemcpyHostToDevice, pl->h2d));
+            HALO_CUDA(cudaMemcpyAsync(sv + kv_layer * l, static_cast<const uint16_t *>(v_new) + kv_layer * l,
+                                      kv_layer * 2, cudaMemcpyHostToDevice, pl->h2d));
+        }
+        if (q_host)
+            HALO_CUDA(cudaMemcpyAsync(static_cast<uint16_t *>(pl->q_stage) + q_layer * l,
+                                      static_cast<const uint16_t *>(q) + q_layer * l, q_layer * 2,
+                                      cudaMemcpyHostToDevice, pl->h2d));
+        HALO_CUDA(cudaEventRecord(pl->ev_in[l], pl->h2d));
+    }
+    const uint16_t *dk = kv_host ? sk : static_cast<const uint16_t *>(k_new);
+    const uint16_t *dv = kv_host ? sv : static_cast<const uint16_t *>(v_new);
+    const uint16_t *dq = q_host ? static_cast<const uint16_t *>(pl->q_stage) : static_cast<const uint16_t *>(q);
+    float *dout = o_host ? pl->o_stage : out;
+    float *dlse = l_host ? pl->l_stage : lse;
+    for (int l = 0; l < L; ++l) {
+        HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_in[l], 0));
+        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk + kv_layer * l, dv + kv_layer * l, nreq,
+                                          pl->slot_stage, nreq, 0, l, l + 1, p->num_sms, s);
+        if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
+        st = run_layer(pl, l, dq + q_layer * l, dout + q_layer * l, dlse ? dlse + rows * l : nullptr, scale, s);
+        if (st != HALO_OK) return st;
+        HALO_CUDA(cudaEventRecord(pl->ev_out[l], s));
+        if (o_host || l_host) {
+            HALO_CUDA(cudaStreamWaitEvent(pl->d2h, pl->ev_out[l], 0));
+            if (o_host)
+                HALO_CUDA(cudaMemcpyAsync(out + q_layer * l, dout + q_layer * l, q_layer * 4,
+                                          cudaMemcpyDeviceToHost, pl->d2h));
+            if (l_host)
+                HALO_CUDA(cudaMemcpyAsync(lse + rows * l, dlse + rows * l, rows * 4, cudaMemcpyDeviceToHost, pl->d2h));
+        }
+    }
+    // the step is complete in `stream` order once the last download has landed
+    HALO_CUDA(cudaEventRecord(pl->ev_copied, pl->d2h));
+    HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_copied, 0));
+    note_stream(p, s);
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
 halo_status halo_plan_get_info(halo_plan pl, halo_plan_info *info) {
     if (!pl || !info) return fail(HALO_EINVAL, "null argument");
     *info = pl->info;
@@ -1317,6 +1468,16 @@ halo_status halo_plan_destroy(halo_plan pl) {
         if (pl->q_stage) cudaFree(pl->q_stage);
         if (pl->o_stage) cudaFree(pl->o_stage);
         if (pl->l_stage) cudaFree(pl->l_stage);
+        pl->pin_plan.release();
+        pl->pin_slots.release();
+        if (pl->kv_stage) cudaFree(pl->kv_stage);
+        if (pl->slot_stage) cudaFree(pl->slot_stage);
+        for (cudaEvent_t e : pl->ev_in) cudaEventDestroy(e);
+        for (cudaEvent_t e : pl->ev_out) cudaEventDestroy(e);
+        if (pl->ev_step) cudaEventDestroy(pl->ev_step);
+        if (pl->ev_copied) cudaEventDestroy(pl->ev_copied);
+        if (pl->h2d) cudaStreamDestroy(pl->h2d);
+        if (pl->d2h) cudaStreamDestroy(pl->d2h);
     }
     p->plans_alive--;
     delete pl;

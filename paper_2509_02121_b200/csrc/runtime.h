@@ -40,6 +40,55 @@ struct StreamFence {
     uint64_t last_use;
 };
 
+// Double-buffered pinned host staging for small per-step uploads (plan arrays, slot lists):
+// an H2D copy from pinned memory is truly asynchronous, so the host can build the next
+// step's plan while the GPU still runs this one.  acquire() waits for the copy that last
+// used the buffer, commit() enqueues the copy and records the buffer's event.
+struct PinRing {
+    void *buf[2] = {nullptr, nullptr};
+    size_t cap[2] = {0, 0};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool used[2] = {false, false};
+    int cur = 0;
+    void *acquire(size_t bytes);                                   // nullptr on failure
+    cudaError_t commit(void *dst, size_t bytes, cudaStream_t s);   // copies buf[cur] -> dst
+    void release();
+};
+
+inline void *PinRing::acquire(size_t bytes) {
+    cur ^= 1;
+    if (used[cur] && ev[cur]) cudaEventSynchronize(ev[cur]);
+    if (!ev[cur] && cudaEventCreateWithFlags(&ev[cur], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    if (cap[cur] < bytes) {
+        if (buf[cur]) cudaFreeHost(buf[cur]);
+        buf[cur] = nullptr;
+        cap[cur] = 0;
+        const size_t c = bytes + bytes / 2 + 4096;
+        if (cudaMallocHost(&buf[cur], c) != cudaSuccess) return nullptr;
+        cap[cur] = c;
+    }
+    return buf[cur];
+}
+
+inline cudaError_t PinRing::commit(void *dst, size_t bytes, cudaStream_t s) {
+    cudaError_t e = bytes ? cudaMemcpyAsync(dst, buf[cur], bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    if (e == cudaSuccess) e = cudaEventRecord(ev[cur], s);
+    used[cur] = (e == cudaSuccess);
+    return e;
+}
+
+inline void PinRing::release() {
+    for (int i = 0; i < 2; ++i) {
+        if (ev[i]) cudaEventSynchronize(ev[i]);
+        if (buf[i]) cudaFreeHost(buf[i]);
+        if (ev[i]) cudaEventDestroy(ev[i]);
+        buf[i] = nullptr;
+        ev[i] = nullptr;
+        cap[i] = 0;
+        used[i] = false;
+    }
+}
+
 }  // namespace halo
 
 struct halo_pool_s {
@@ -81,7 +130,8 @@ struct halo_plan_s {
     std::vector<int32_t> unit_meta;   // [U][8] K2 unit metadata (PlanDev::unit_meta)
     std::vector<halo::PrefixTile> tiles;
     halo_plan_info info{};
-    std::vector<uint8_t> host_buf;
+    std::vector<uint8_t> host_buf;   // host-only pools
+    halo::PinRing pin_plan, pin_slots;
     void *dbuf = nullptr;
     size_t dbuf_cap = 0;
     float *part = nullptr;
@@ -98,4 +148,12 @@ struct halo_plan_s {
     size_t o_stage_cap = 0;
     float *l_stage = nullptr;
     size_t l_stage_cap = 0;
+    // halo_decode_step: copy streams, per-layer events and the appended token's K/V staging
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_out;
+    cudaEvent_t ev_step = nullptr, ev_copied = nullptr;
+    void *kv_stage = nullptr;
+    size_t kv_stage_cap = 0;
+    int32_t *slot_stage = nullptr;
+    size_t slot_stage_cap = 0;
 };

@@ -259,3 +259,69 @@ def test_truncate_then_append_is_a_stationary_step():
     torch.cuda.synchronize()
     assert np.array_equal(o2.cpu().numpy(), out[0])
     cleanup(ld, plan)
+
+
+def _decode_step_outputs(wl, host: bool):
+    ld = load(wl, DEV)
+    nk, nv = wl.new_kv(0, f"cuda:{DEV}")
+    q = wl.q(0, f"cuda:{DEV}")
+    L = wl.layers
+    if host:
+        nk, nv, q = nk.cpu().pin_memory(), nv.cpu().pin_memory(), q.cpu().pin_memory()
+        out = torch.full((L, wl.nreq, wl.hq, wl.d), float("nan")).pin_memory()
+        lse = torch.full((L, wl.nreq, wl.hq), float("nan")).pin_memory()
+    else:
+        out = torch.full((L, wl.nreq, wl.hq, wl.d), float("nan"), device=f"cuda:{DEV}")
+        lse = torch.full((L, wl.nreq, wl.hq), float("nan"), device=f"cuda:{DEV}")
+    plan = ld.pool.decode_step(ld.req_ids, nk, nv, q, out, lse)
+    torch.cuda.synchronize()
+    o, l_ = out.cpu().numpy(), lse.cpu().numpy()
+    return ld, plan, o, l_
+
+
+@pytest.mark.parametrize("host", [True, False])
+def test_decode_step_pipelined_matches_oracle_and_run(host):
+    """halo_decode_step (append + plan + every layer, copies overlapped per layer) equals the
+    oracle and is bit-identical to append + plan + halo_decode_run."""
+    wl = make_config("ragged", layers=3)
+    ld, plan, o, l_ = _decode_step_outputs(wl, host)
+    for layer in range(wl.layers):
+        ro, rl = oracle.decode_reference(wl, layer, steps=1)
+        assert np.abs(o[layer] - ro).max() <= OUT_TOL
+        assert np.abs(l_[layer] - rl).max() <= LSE_TOL
+    cleanup(ld, plan)
+    ld2, plan2, o2, l2 = run_step(wl)
+    assert np.array_equal(o, o2) and np.array_equal(l_, l2)
+    cleanup(ld2, plan2)
+
+
+def test_decode_step_reuses_its_plan_across_steps():
+    wl = make_config("fanout", layers=2, nreq=48, prefix=200, suffix=14)
+    ld = load(wl, DEV)
+    L = wl.layers
+    outs = []
+    plan = None
+    for step in range(3):
+        nk, nv = wl.new_kv(step, "cuda")
+        q = wl.q(step, "cuda")
+        out = torch.empty((L, wl.nreq, wl.hq, wl.d), device="cuda")
+        plan = ld.pool.decode_step(ld.req_ids, nk, nv, q, out, reuse=plan)
+        outs.append(out)
+    torch.cuda.synchronize()
+    for layer in range(L):
+        ro, _ = oracle.decode_reference(wl, layer, steps=3)
+        assert np.abs(outs[2][layer].cpu().numpy() - ro).max() <= OUT_TOL
+    cleanup(ld, plan)
+
+
+def test_full_c2_tree_sampled_at_bench_configuration():
+    """C2 (BASELINE configs[2]): 4k root -> 16 x 1k roles -> 1024 requests, two prefix levels
+    merged with the suffix; the per-layer shapes bench.py's other_configs leg times."""
+    wl = make_config("tree", layers=2)
+    check(wl, layers=[1], sample=[0, 63, 64, 500, 1023])
+
+
+def test_full_c3_analytics_sampled_at_bench_configuration():
+    """C3 per GPU (BASELINE configs[3]): 8 templates x 8k-token contexts x 256 requests."""
+    wl = make_config("analytics", layers=1)
+    check(wl, layers=[0], sample=[0, 255, 256, 1100, 2047])

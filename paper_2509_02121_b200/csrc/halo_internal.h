@@ -57,6 +57,7 @@ struct PlanDev {
     // unit_meta[2u], [2u+1] = {boff_begin, boff_end, request, kv head},
     //                         {nslots, nseg, first seg slot, first chunk}.
     const uint2 *k2_ent;         // [nblocks]
+    const int4 *chunk_info;      // [nchunks] {chunk_lo[c], chunk_lo[c+1], chunk_u0[c], chunk_u1[c]}
     const int4 *unit_meta;       // [2 * nunits]
     const int32_t *unit_boff;    // [nunits + 1]
     const int32_t *chunk_lo;     // [nchunks + 1]

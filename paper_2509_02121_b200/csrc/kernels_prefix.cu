@@ -122,6 +122,9 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + C::OFF_BAR + C::NBAR * 8);
 
     if (threadIdx.x == 0) K1_TRACE(9, 0);
+    // PDL: let K2 (the next kernel: streams private suffixes, reads our partials only after
+    // griddepcontrol.wait) start on SMs this grid leaves idle and as its CTAs retire
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const PrefixTile T = a.p.tiles[blockIdx.x];
     const int NT = (T.tok_end - T.tok_begin + kK1Tok - 1) / kK1Tok;
     const bool hasB = T.nrows > kSubRows;

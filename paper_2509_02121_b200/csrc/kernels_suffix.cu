@@ -222,10 +222,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     const uint16_t *pv = a.pool_v + a.layer_off;
 
     // ---- producer (all lanes track the state; lane 0 issues the copies) ----
+    // PDL: the next kernel in the stream (the next layer's K1) may start its prologue now;
+    // it waits (griddepcontrol.wait) for this grid before touching anything K2 reads.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     int pch = gw, px = 0, phi = 0, pstart = 0;
+    int4 ci = make_int4(0, 0, 0, 0);
     if (pch < P.nchunks) {
-        px = pstart = P.chunk_lo[pch];
-        phi = P.chunk_lo[pch + 1];
+        ci = P.chunk_info[pch];
+        px = pstart = ci.x;
+        phi = ci.y;
     }
     uint32_t p_count = 0, c_count = 0, q_issued = 0, q_read = 0;
     int eb = -64;                       // base index of the descriptor batch in `ent`
@@ -239,8 +244,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 if (pch >= P.nchunks) break;
                 pch += P.nwarps;
                 if (pch >= P.nchunks) break;
-                px = pstart = P.chunk_lo[pch];
-                phi = P.chunk_lo[pch + 1];
+                const int4 c2 = P.chunk_info[pch];
+                px = pstart = c2.x;
+                phi = c2.y;
                 continue;
             }
             if (px - eb >= 32 || px < eb) {
@@ -279,9 +285,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     };
     fill();
 
+    // K1's partials (this layer's prefix attention) are read only in the epilogue and this
+    // grid writes nothing before it: the streaming of the first unit piece may overlap K1
+    // under programmatic dependent launch (griddepcontrol.wait before the first write).
+    bool k1_ready = false;
+    auto wait_k1 = [&]() {
+        if (!k1_ready) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            k1_ready = true;
+        }
+    };
     for (int cc = gw; cc < P.nchunks; cc += P.nwarps) {
-        const int lo = P.chunk_lo[cc], hi = P.chunk_lo[cc + 1];
-        const int u_begin = P.chunk_u0[cc], u_end = P.chunk_u1[cc];
+        const int4 cinfo = cc == gw ? ci : P.chunk_info[cc];
+        const int lo = cinfo.x, hi = cinfo.y;
+        const int u_begin = cinfo.z, u_end = cinfo.w;
         for (int u = u_begin; u < u_end; ++u) {
             const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
             const int xs = max(m0.x, lo), xe = min(m0.y, hi);
@@ -453,6 +470,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 lh[h] = __shfl_sync(0xffffffffu, l, h * (LPT / G));
             }
             const int nslots = m1.x, nseg = m1.y;
+            // first global write of this grid: the previous kernel(s) must be complete
+            wait_k1();
             if (nseg == 1) {
                 finalize<D, G>(a, req, head, nslots, lane, mh, lh, o2);
             } else {
@@ -463,13 +482,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
 #pragma unroll
                 for (int h = 0; h < G; ++h)
                     if (lane == h) *reinterpret_cast<float2 *>(P.seg_ml + ((int64_t)slot * G + h) * 2) = make_float2(mh[h], lh[h]);
-                __threadfence();
+                // one acq_rel arrival by lane 0: release covers the whole warp's stores
+                // (ordered before it by the warp barrier), acquire makes the other pieces'
+                // stores visible to the merging warp (read from L2 with ld.cg)
                 __syncwarp();
                 int old = 0;
-                if (lane == 0) old = atomicAdd(&P.unit_count[u], 1);
+                if (lane == 0)
+                    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                                 : "=r"(old) : "l"(P.unit_count + u) : "memory");
                 old = __shfl_sync(0xffffffffu, old, 0);
                 if (old == nseg - 1) {
-                    __threadfence();
                     if (lane == 0) P.unit_count[u] = 0;  // ready for the next launch
                     // merge all pieces in segment order (deterministic), from L2
                     float M[G], L[G];
@@ -521,8 +543,18 @@ cudaError_t launch_t(const SuffixArgs &a, cudaStream_t s) {
     }
     if (a.p.nunits == 0) return cudaSuccess;
     const int grid = (a.p.nwarps + kWarps - 1) / kWarps;  // = num_sms: one CTA per SM
-    kern<<<grid, kWarps * 32, smem, s>>>(a);
-    return cudaGetLastError();
+    // programmatic dependent launch: CTAs may start while K1 (the previous kernel) drains
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.p.ntiles > 0 ? 1 : 0;  // overlap K1 only (never a previous K2)
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 }  // namespace

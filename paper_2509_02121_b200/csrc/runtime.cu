@@ -582,6 +582,13 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
         for (int64_t cc = 0; cc < nchunks; ++cc)
             if (pl->chunk_u0[cc] >= pl->chunk_u1[cc]) pl->chunk_u0[cc] = pl->chunk_u1[cc] = 0;
         pl->nseg_total = nseg_total;
+        pl->chunk_info.resize((size_t)nchunks * 4);
+        for (int64_t cc = 0; cc < nchunks; ++cc) {
+            pl->chunk_info[4 * cc] = lo[cc];
+            pl->chunk_info[4 * cc + 1] = lo[cc + 1];
+            pl->chunk_info[4 * cc + 2] = pl->chunk_u0[cc];
+            pl->chunk_info[4 * cc + 3] = pl->chunk_u1[cc];
+        }
         // per-block descriptors and per-unit metadata read by the kernel
         pl->k2_ent.resize((size_t)Btot * 2);
         pl->unit_meta.resize((size_t)U * 8);
@@ -644,6 +651,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const size_t o_useg = off; off = align16(off + U * 4);
     const size_t o_ent = off; off = align16(off + pl->k2_ent.size() * 4);
     const size_t o_umeta = off; off = align16(off + pl->unit_meta.size() * 4);
+    const size_t o_cinfo = off; off = align16(off + pl->chunk_info.size() * 4);
     const size_t total = off;
     uint8_t *h;
     if (p->host_only) {
@@ -670,6 +678,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     put(o_useg, pl->unit_seg.data(), U * 4);
     put(o_ent, pl->k2_ent.data(), pl->k2_ent.size() * 4);
     put(o_umeta, pl->unit_meta.data(), pl->unit_meta.size() * 4);
+    put(o_cinfo, pl->chunk_info.data(), pl->chunk_info.size() * 4);
     if (p->host_only) return HALO_OK;
 
     if (pl->dbuf_cap < total) {
@@ -738,6 +747,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     dv.unit_count = pl->counters;
     dv.k2_ent = reinterpret_cast<const uint2 *>(d + o_ent);
     dv.unit_meta = reinterpret_cast<const int4 *>(d + o_umeta);
+    dv.chunk_info = reinterpret_cast<const int4 *>(d + o_cinfo);
     dv.nchunks = NC;
     dv.nblocks = pl->unit_boff.empty() ? 0 : pl->unit_boff.back();
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;

@@ -37,6 +37,8 @@ UNIT = "queries/s"
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
 FALLBACK_BF16_TFLOPS = 1590.0
 NVLINK_PEER_GBS = 770.0     # B200_PROFILING.md: measured peer copy per direction
+TIMING_NOTE = ("CUDA events on the launching stream around every launch of the kernel, averaged "
+               "over the K-step breakdown pass (same workload, right after the headline pass)")
 
 
 def peaks():
@@ -212,50 +214,56 @@ def setup_workload(halo, wl, dev, torch):
         pool.append(reqs, ones, nk, nv)
         pool.plan(reqs, popt, reuse=plan)
         for l in range(L):
-            if evs is not None:
-                evs[l][0].record(stream)
+            if evs is None:                       # headline pass: K1 -> K2 back to back (PDL)
+                plan.run(l, q[l], out[l], lse[l])
+                continue
+            evs[l][0].record(stream)              # breakdown pass: an event around each kernel
             plan.run_stages(l, 1, q[l], out[l], lse[l])
-            if evs is not None:
-                evs[l][1].record(stream)
+            evs[l][1].record(stream)
             plan.run_stages(l, 2, q[l], out[l], lse[l])
-            if evs is not None:
-                evs[l][2].record(stream)
+            evs[l][2].record(stream)
     return ld, plan, info, step, (nk, nv, q, out, lse, ones, popt)
 
 
 def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=False):
-    """W untimed steps, then K timed steps between barriers + syncs (CUDA events on the
-    launching stream); per-kernel times from events around each K1 / K2 launch.  Max over
-    ranks."""
+    """W untimed steps, then two timed passes of K steps, each between barriers + syncs with
+    CUDA events on the launching stream, max over ranks:
+      1. the headline pass: whole steps only (K1 and K2 of a layer back to back, so K2's
+         programmatic dependent launch overlaps K1's tail);
+      2. the breakdown pass: an event before K1, between K1 and K2 and after K2 of every
+         layer (per-kernel launch durations for the rooflines; the events serialise the
+         kernels, so this pass is a little slower than the first).
+    Returns (pass-1 ms, pass-2 ms, pass-2 K1 ms, pass-2 K2 ms, clock sampler)."""
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)]
            for _ in range(steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    t = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     clk = ClockSampler(dev) if sample_clocks else None
     if clk:
         clk.__enter__()
-    t_start.record(stream)
-    for s in range(steps):
-        step(evs[s])
-    t_end.record(stream)
-    torch.cuda.synchronize()
+    for p in range(2):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t[2 * p].record(stream)
+        for s in range(steps):
+            step(evs[s] if p == 1 else None)
+        t[2 * p + 1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     if clk:
         clk.__exit__()
-    if world > 1:
-        dist.barrier()
-    ms = t_start.elapsed_time(t_end)
+    ms, ms_bd = t[0].elapsed_time(t[1]), t[2].elapsed_time(t[3])
     k1_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st)
     k2_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st)
     from paper_2509_02121_b200.sharding import max_over_ranks
-    ms, k1_ms, k2_ms = max_over_ranks([ms, k1_ms, k2_ms], dist if world > 1 else None,
-                                      f"cuda:{dev}")
-    return ms, k1_ms, k2_ms, clk
+    ms, ms_bd, k1_ms, k2_ms = max_over_ranks([ms, ms_bd, k1_ms, k2_ms], dist if world > 1 else None,
+                                             f"cuda:{dev}")
+    return ms, ms_bd, k1_ms, k2_ms, clk
 
 
 def kernel_rooflines(info, k1_launch_ms, k2_launch_ms):
@@ -265,11 +273,11 @@ def kernel_rooflines(info, k1_launch_ms, k2_launch_ms):
     return ({"bound": "hbm", "kernel": "suffix_decode_kernel (K2+K3)", "achieved": k2_gbs,
              "peak": hbm_peak, "unit": "GB/s", "frac": k2_gbs / hbm_peak,
              "algorithmic_bytes_per_launch": info["k2_bytes"], "avg_launch_ms": k2_launch_ms,
-             "peak_source": peak_src},
+             "timing": TIMING_NOTE, "peak_source": peak_src},
             {"bound": "tensor", "kernel": "prefix_attn_kernel (K1)", "achieved": k1_tflops,
              "peak": tc_peak, "unit": "TFLOP/s", "frac": (k1_tflops / tc_peak) if k1_tflops else None,
              "algorithmic_flops_per_launch": info["k1_flops"], "avg_launch_ms": k1_launch_ms,
-             "peak_source": peak_src})
+             "timing": TIMING_NOTE, "peak_source": peak_src})
 
 
 def measure_other_configs(halo, names, layers, steps, warmup, world, dev, torch, dist):
@@ -281,7 +289,7 @@ def measure_other_configs(halo, names, layers, steps, warmup, world, dev, torch,
     for name in names:
         wl = make_config(name, layers=layers)
         ld, plan, info, step, bufs = setup_workload(halo, wl, dev, torch)
-        ms, k1_ms, k2_ms, _ = time_steps(step, wl.layers, steps, warmup, world, dev, torch, dist)
+        ms, _, k1_ms, k2_ms, _ = time_steps(step, wl.layers, steps, warmup, world, dev, torch, dist)
         n = steps * wl.layers
         k2r, k1r = kernel_rooflines(info, k1_ms / n, k2_ms / n)
         layer_ms = (k1_ms + k2_ms) / n
@@ -338,7 +346,7 @@ def main():
     ld, plan, info, step, (nk, nv, q, out, lse, ones, popt) = setup_workload(halo, wl, dev, torch)
     pool, reqs = ld.pool, ld.req_ids
     stream = torch.cuda.current_stream()
-    ms, k1_ms, k2_ms, clk = time_steps(step, L, args.steps, args.warmup, world, dev, torch, dist,
+    ms, ms_bd, k1_ms, k2_ms, clk = time_steps(step, L, args.steps, args.warmup, world, dev, torch, dist,
                                        sample_clocks=True)
     launches = args.steps * (1 + 2 * L)
     ms_step = ms / args.steps
@@ -412,8 +420,10 @@ def main():
                        "k1_tiles": info["k1_tiles"], "k2_units": info["k2_units"]},
             "roofline": dict(k2_roof, traffic=traffic),
             "prefix_roofline": k1_roof,
-            "step_breakdown_ms": {"k1": k1_ms / args.steps, "k2": k2_ms / args.steps,
-                                  "other": ms_step - (k1_ms + k2_ms) / args.steps},
+            "step_breakdown_ms": {"pass": "breakdown pass (events around each kernel)",
+                                  "step": ms_bd / args.steps, "k1": k1_ms / args.steps,
+                                  "k2": k2_ms / args.steps,
+                                  "other": (ms_bd - k1_ms - k2_ms) / args.steps},
             "unshared_bytes_per_layer": info["unshared_bytes"],
             "gpu_launches": launches,
             "clocks": clk.summary(),

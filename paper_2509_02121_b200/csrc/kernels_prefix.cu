@@ -167,6 +167,9 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         const int nblk = (T.tok_end + kBlockTok - 1) / kBlockTok - blk_first;
         for (int i = lane; i < nblk; i += 32) blocks[i] = a.p.node_blocks[T.blk_off + blk_first + i];
         __syncwarp();
+        // PDL: this grid may start while the previous kernel drains; the pool blocks it reads
+        // may have been written by that kernel (a registration or append), so wait here
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         if (lane == 0) {
             ptx::prefetch_tmap(&tmk);
             ptx::prefetch_tmap(&tmv);
@@ -300,7 +303,9 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         const int g = a.g;
         const int req = valid_row ? a.p.req_order[T.req_off + trow / g] : 0;
         const int head = T.kv_head * g + trow % g;
-        // Q row -> smem, K-major SW128 (16-B chunk c of row r lands at chunk c ^ (r & 7))
+        // Q row -> smem, K-major SW128 (16-B chunk c of row r lands at chunk c ^ (r & 7)).
+        // q and the partials (read by the previous layer's K2) belong to earlier kernels.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.q + ((int64_t)req * a.hq + head) * D);
             uint8_t *qs = sm + C::OFF_Q + x * C::Q_BYTES;
@@ -468,8 +473,19 @@ cudaError_t launch_t(const CUtensorMap *tmk, const CUtensorMap *tmv, const CUten
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    kern<<<a.p.ntiles, kThreads, L1<D>::SMEM, s>>>(*tmk, *tmv, *tmk8, *tmv8, a);
-    return cudaGetLastError();
+    // programmatic dependent launch: barrier init, TMEM allocation and the tile's block list
+    // overlap the previous kernel's tail (griddepcontrol.wait before any dependent access)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.p.ntiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = L1<D>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, *tmk, *tmv, *tmk8, *tmv8, a);
 }
 
 }  // namespace

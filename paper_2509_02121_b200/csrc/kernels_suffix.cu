@@ -150,7 +150,8 @@ __device__ __forceinline__ void st_pairs(float *p, const float2 (&x)[NP], float 
 // [lane*D/32, (lane+1)*D/32) of the G heads.
 template <int D, int G>
 __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head, int nslots, int lane,
-                                         const float (&mh)[G], const float (&lh)[G], OAcc<D, G> &o2) {
+                                         const float (&mh)[G], const float (&lh)[G], OAcc<D, G> &o2,
+                                         const float (&lse0)[G], bool have0) {
     constexpr int NP = D / 64, DPL = D / 32;
     const PlanDev &P = a.p;
     float M[G], L[G];
@@ -160,7 +161,8 @@ __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head,
     const int64_t row0 = (int64_t)req * a.hq + head * G;
     for (int sl = 0; sl < nslots; ++sl) {
 #pragma unroll
-        for (int h = 0; h < G; ++h) M[h] = fmaxf(M[h], P.part_lse[sl * slot_stride + row0 + h] * kLog2e);
+        for (int h = 0; h < G; ++h)
+            M[h] = fmaxf(M[h], (sl == 0 && have0 ? lse0[h] : P.part_lse[sl * slot_stride + row0 + h]) * kLog2e);
     }
 #pragma unroll
     for (int h = 0; h < G; ++h) {
@@ -173,7 +175,7 @@ __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head,
 #pragma unroll
         for (int h = 0; h < G; ++h) {
             const int64_t row = sl * slot_stride + row0 + h;
-            const float w = ptx::ex2(P.part_lse[row] * kLog2e - M[h]);
+            const float w = ptx::ex2((sl == 0 && have0 ? lse0[h] : P.part_lse[row]) * kLog2e - M[h]);
             L[h] += w;
             float2 x[NP];
             ld_pairs<NP>(P.part_o + row * D + lane * DPL, x);
@@ -303,6 +305,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
             const int xs = max(m0.x, lo), xe = min(m0.y, hi);
             const int req = m0.z, head = m0.w;
+            // once K1 is known complete, the merge's first partial lse is loaded now and
+            // lands while the unit streams (the merge otherwise waits one L2 round trip)
+            float lse0[G];
+            const bool have0 = k1_ready && m1.x > 0 && m1.y == 1;
+            if (have0) {
+                const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
+#pragma unroll
+                for (int h = 0; h < G; ++h) lse0[h] = __ldcg(src + h);
+            } else {
+#pragma unroll
+                for (int h = 0; h < G; ++h) lse0[h] = 0.f;
+            }
             OAcc<D, G> o2;
 #pragma unroll
             for (int h = 0; h < G; ++h)
@@ -473,7 +487,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             // first global write of this grid: the previous kernel(s) must be complete
             wait_k1();
             if (nseg == 1) {
-                finalize<D, G>(a, req, head, nslots, lane, mh, lh, o2);
+                finalize<D, G>(a, req, head, nslots, lane, mh, lh, o2, lse0, have0);
             } else {
                 // ---- stream-K: publish this piece's state; the last piece merges them all ----
                 const int slot = m1.z + (cc - m1.w);
@@ -493,7 +507,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 old = __shfl_sync(0xffffffffu, old, 0);
                 if (old == nseg - 1) {
                     if (lane == 0) P.unit_count[u] = 0;  // ready for the next launch
-                    // merge all pieces in segment order (deterministic), from L2
+                    // merge all pieces in segment order (deterministic), from L2; the first
+                    // K1 partial lse is requested up front so its latency overlaps the merge
+                    float lseM[G];
+                    const bool haveM = nslots > 0;
+                    {
+                        const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
+#pragma unroll
+                        for (int h = 0; h < G; ++h) lseM[h] = haveM ? __ldcg(src + h) : 0.f;
+                    }
                     float M[G], L[G];
 #pragma unroll
                     for (int h = 0; h < G; ++h) { M[h] = -INFINITY; L[h] = 0.f; }
@@ -519,7 +541,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                             for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(w, w), x[i], o2[h][i]);
                         }
                     }
-                    finalize<D, G>(a, req, head, nslots, lane, M, L, o2);
+                    finalize<D, G>(a, req, head, nslots, lane, M, L, o2, lseM, haveM);
 
                 }
             }

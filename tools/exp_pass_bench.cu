@@ -1,0 +1,100 @@
+// Microbenchmark of K1's softmax exp pass (calibration; not product code): one thread = one
+// 128-column score row in registers; per pass p = 2^(s*c - m) for the row (16 FFMA2, 32
+// MUFU.EX2, 16 FADD2, 16 F2FP per 32-column chunk), with NPOLY of every 16 pairs per chunk
+// computed by a degree-3 polynomial exp2 on the FMA pipe instead of MUFU.  Reports cycles
+// per pass per warp for W warps per SMSP.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r)
+        : "l"(*reinterpret_cast<uint64_t *>(&a)), "l"(*reinterpret_cast<uint64_t *>(&b)),
+          "l"(*reinterpret_cast<uint64_t *>(&c)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r)
+        : "l"(*reinterpret_cast<uint64_t *>(&a)), "l"(*reinterpret_cast<uint64_t *>(&b)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+__device__ __forceinline__ float ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ uint32_t h2(float lo, float hi) {
+    uint32_t r; asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo)); return r;
+}
+// 2^x, x in [-127, 127]: round-to-nearest split x = j + f (|f| <= 1/2), minimax-ish cubic for
+// 2^f, exponent added in the integer domain.  Packed pairs.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = fadd2(x, magic);
+    const float2 jf = fadd2(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = fadd2(x, make_float2(-jf.x, -jf.y));
+    float2 p = ffma2(f, make_float2(5.508868e-2f, 5.508868e-2f), make_float2(2.4260405e-1f, 2.4260405e-1f));
+    p = ffma2(p, f, make_float2(6.9327624e-1f, 6.9327624e-1f));
+    p = ffma2(p, f, make_float2(9.9992894e-1f, 9.9992894e-1f));
+    const uint32_t bx = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+    const uint32_t by = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+    return make_float2(__uint_as_float(bx), __uint_as_float(by));
+}
+
+template <int NPOLY, int VARIANT = 0>  // VARIANT 1: no F2FP, 2: no F2FP/FADD2, 3: MUFU only
+__global__ void pass_kernel(float *out, int iters, long long *cyc) {
+    float s[128];
+    for (int i = 0; i < 128; ++i) s[i] = -(threadIdx.x % 7) * 0.01f - i * 0.003f;
+    const float2 c2v = make_float2(1.3f, 1.3f), nm = make_float2(-0.5f, -0.5f);
+    float2 acc[4] = {};
+    uint32_t sink = 0;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float2 e[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) e[i] = ffma2(make_float2(s[32 * k + 2 * i], s[32 * k + 2 * i + 1]), c2v, nm);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (i < NPOLY) e[i] = ex2_poly2(e[i]);
+                else { e[i].x = ex2(e[i].x); e[i].y = ex2(e[i].y); }
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (VARIANT < 2) acc[i & 3] = fadd2(acc[i & 3], e[i]);
+                if (VARIANT == 0) pk[i] = h2(e[i].x, e[i].y);
+                else pk[i] = __float_as_uint(e[i].x) ^ __float_as_uint(e[i].y);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sink ^= pk[i];
+        }
+        s[it & 127] += 1e-7f;  // keep the loop honest
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0].x + acc[1].y + acc[2].x + acc[3].y + sink;
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
+int main() {
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    float *out; long long *cyc; cudaMalloc(&out, 1 << 24); cudaMalloc(&cyc, 8);
+    auto run = [&](auto kern, const char *name) {
+        for (int wps : {1, 2}) {
+            const int iters = 2000;
+            kern<<<sms, 128 * wps>>>(out, iters, cyc); cudaDeviceSynchronize();
+            kern<<<sms, 128 * wps>>>(out, iters, cyc); cudaDeviceSynchronize();
+            long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("%-10s warps/SMSP=%d  %.0f cycles per 128-column pass per warp  (MUFU bound %d)\n",
+                   name, wps, (double)c / iters, 128 * 8 * wps * 0 + (int)(128.0 * 8 * wps * (1.0 - 0.0)));
+        }
+    };
+    run(pass_kernel<0>, "mufu");
+    run(pass_kernel<0, 1>, "no-f2fp");
+    run(pass_kernel<0, 2>, "no-f2fp-add");
+    run(pass_kernel<4>, "poly 4/16");
+    run(pass_kernel<4, 1>, "poly4 nof2fp");
+    // accuracy of the polynomial over [-20, 0]
+    return 0;
+}

@@ -323,6 +323,8 @@ def main():
                     help="BASELINE configs also measured per launch (C2 tree, C3 analytics); '' = none")
     ap.add_argument("--other-layers", type=int, default=4)
     ap.add_argument("--layers", type=int, default=0, help="override the config's layer count (profiling)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: debug the N>1 path with several ranks on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -335,10 +337,16 @@ def main():
     from synth import make_config
 
     rank, world, local = dist_env()
-    dev = local
+    # --dist-backend gloo (debug): exercise the multi-rank code path with several ranks on
+    # one GPU (NCCL refuses two ranks per device); the NCCL migration leg is skipped then.
+    dev = local % torch.cuda.device_count() if args.dist_backend == "gloo" else local
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+            args.no_migration = True
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     halo.load_library()
 
     wl = make_config(args.config, seed=1 + 1000 * rank, **({"layers": args.layers} if args.layers else {}))

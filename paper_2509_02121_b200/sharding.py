@@ -110,6 +110,8 @@ def max_over_ranks(values, dist=None, device=None) -> list:
     if dist is None or not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return list(values)
     import torch
+    if dist.get_backend() == "gloo":
+        device = "cpu"
     t = torch.tensor(list(values), dtype=torch.float64, device=device or "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()

@@ -401,6 +401,9 @@ def main():
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
         extra["migration"] = measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist)
+    # ---- host paging of the template node (NEXT-2) ----
+    if not args.no_migration and not args.profile:
+        extra["paging"] = measure_paging(pool, ld, wl, torch)
     # ---- per-launch rooflines on the other configs (C2, C3) ----
     if args.other_configs and not args.profile:
         extra["other_configs"] = measure_other_configs(
@@ -442,6 +445,65 @@ def main():
     pool.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_paging(pool, ld, wl, torch):
+    """Offload (D2H) and fetch (H2D) of the C1 template node (256 MiB of K+V) through the
+    library's pinned host arena (halo_prefix_offload / halo_prefix_fetch), CUDA events on the
+    stream; the denominator is a plain pinned cudaMemcpy of the same bytes in this run.  The
+    transfer-vs-recompute line is a derived estimate (prefill FLOPs of the 2048-token prefix
+    through Llama-3-8B, 2 x 8.0e9 x tokens, at the measured bf16 peak), not a measurement."""
+    node = ld.node_ids[0]
+    ntok = wl.nodes[0].ntok
+    nbytes = ntok * wl.layers * wl.hkv * wl.d * 2 * 2
+    stream = torch.cuda.current_stream()
+    pool.host_reserve((ntok + 15) // 16)
+
+    def timed(fn, reps=3):
+        best = None
+        for i in range(reps + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i:
+                best = e0.elapsed_time(e1) if best is None else min(best, e0.elapsed_time(e1))
+        return best
+    t_off = t_fetch = None
+    for _ in range(3):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        pool.offload_prefix(node, stream)
+        e1.record(stream)
+        pool.fetch_prefix(node, stream)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        a, b = e0.elapsed_time(e1), e1.elapsed_time(e2)
+        t_off = a if t_off is None else min(t_off, a)
+        t_fetch = b if t_fetch is None else min(t_fetch, b)
+    h = torch.empty(nbytes // 4, pin_memory=True)
+    d = torch.empty(nbytes // 4, device=stream.device)
+    d2h = timed(lambda: h.copy_(d, non_blocking=True))
+    h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    del h, d
+    pool.host_reserve(0)
+    _, tc_peak, _, _ = peaks()
+    prefill_ms = 2 * 8.0e9 * ntok / (tc_peak * 1e12) * 1e3
+    return {"what": "halo_prefix_offload / halo_prefix_fetch of the C1 template node (K+V, 32 layers)",
+            "bytes": nbytes,
+            "offload": {"ms": t_off, "GB/s": nbytes / t_off / 1e6,
+                        "pcie_roofline": {"bound": "pcie", "achieved": nbytes / t_off / 1e6,
+                                          "peak": nbytes / d2h / 1e6, "unit": "GB/s",
+                                          "frac": d2h / t_off,
+                                          "peak_source": "pinned cudaMemcpy D2H of the same bytes, this run"}},
+            "fetch": {"ms": t_fetch, "GB/s": nbytes / t_fetch / 1e6,
+                      "pcie_roofline": {"bound": "pcie", "achieved": nbytes / t_fetch / 1e6,
+                                        "peak": nbytes / h2d / 1e6, "unit": "GB/s",
+                                        "frac": h2d / t_fetch,
+                                        "peak_source": "pinned cudaMemcpy H2D of the same bytes, this run"}},
+            "recompute_estimate_ms": prefill_ms,
+            "transfer_vs_recompute": prefill_ms / t_fetch}
 
 
 def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):

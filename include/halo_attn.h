@@ -243,6 +243,37 @@ halo_status halo_migrate_recv(halo_pool pool, int32_t src_rank, int64_t parent, 
 halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_t parent_dst,
                               void *stream, int64_t *node_out);
 
+/* ------------------------------------------------------------------ host paging
+ * The executor's I/O subsystem "asynchronously pages activation caches between GPU and host
+ * memory ... prefetch upcoming caches and evict stale ones under the scheduler's control"
+ * (PAPER.md:350 §3.3; snapshots "offloaded to host memory under scheduler control", :337).
+ * A prefix node is either device-resident (its blocks in the pool) or offloaded (its KV in
+ * blocks of a pinned host arena, same [layer][block][head][16][d] layout).  Offload / fetch
+ * are stream-ordered copies on the copy engines (one cudaMemcpyAsync per run of consecutive
+ * blocks per layer); the blocks they give up return to their free lists once the enqueued
+ * copy has passed.  Plans that read an offloaded node fail with HALO_EBUSY; a plan built
+ * before an offload / fetch is stale and halo_decode_run returns HALO_EBUSY (re-plan). */
+
+/* (Re)allocate the pinned host arena: host_blocks blocks x all layers x K and V.  EBUSY while
+ * nodes are offloaded; ENOMEM (arena cleared) if the pinned allocation fails.  On a host-only
+ * pool (device -1) this is bookkeeping only (tests). */
+halo_status halo_pool_host_reserve(halo_pool pool, int64_t host_blocks);
+/* Evict: copy the node's blocks to fresh host-arena blocks on `stream`, then release its
+ * device blocks.  ENOENT unknown node; EINVAL already offloaded; EUNSUPPORTED no arena;
+ * ENOMEM arena full (nothing changes). */
+halo_status halo_prefix_offload(halo_pool pool, int64_t node, void *stream);
+/* Prefetch: copy an offloaded node back into fresh device blocks on `stream` (same node id,
+ * tree position and requests).  EINVAL if not offloaded; ENOMEM pool full (nothing
+ * changes). */
+halo_status halo_prefix_fetch(halo_pool pool, int64_t node, void *stream);
+/* on_device: 1 resident, 0 offloaded; last_use: LRU clock of the last plan that read it. */
+halo_status halo_node_residency(halo_pool pool, int64_t node, int32_t *on_device, uint64_t *last_use);
+/* LRU eviction policy: offload device-resident nodes in increasing last_use (ties: lower id),
+ * never one read by the most recent plan, until free + pending-free device blocks >=
+ * want_free.  *n_evicted = nodes offloaded.  ENOMEM if the target cannot be reached (the
+ * evictions made so far stay). */
+halo_status halo_pool_evict_lru(halo_pool pool, int64_t want_free, void *stream, int32_t *n_evicted);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,11 @@ SIGNATURES = {
     "halo_migrate_send": (_i32, [_p, _i64, _i32, _i32, _p]),
     "halo_migrate_recv": (_i32, [_p, _i32, _i64, _i32, _p, _pi64]),
     "halo_prefix_clone": (_i32, [_p, _i64, _p, _i64, _p, _pi64]),
+    "halo_pool_host_reserve": (_i32, [_p, _i64]),
+    "halo_prefix_offload": (_i32, [_p, _i64, _p]),
+    "halo_prefix_fetch": (_i32, [_p, _i64, _p]),
+    "halo_node_residency": (_i32, [_p, _i64, C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]),
+    "halo_pool_evict_lru": (_i32, [_p, _i64, _p, C.POINTER(C.c_int32)]),
 }
 
 _lib = None
@@ -262,6 +267,26 @@ class Pool:
             reuse.nreq = len(reqs)
             return reuse
         return Plan(self, h, len(reqs))
+
+    # ---- host paging ----
+    def host_reserve(self, host_blocks: int):
+        _call("halo_pool_host_reserve", self.handle, host_blocks)
+
+    def offload_prefix(self, node: int, stream=None):
+        _call("halo_prefix_offload", self.handle, node, self._s(stream))
+
+    def fetch_prefix(self, node: int, stream=None):
+        _call("halo_prefix_fetch", self.handle, node, self._s(stream))
+
+    def residency(self, node: int) -> tuple:
+        on, last = C.c_int32(), C.c_uint64()
+        _call("halo_node_residency", self.handle, node, C.byref(on), C.byref(last))
+        return bool(on.value), int(last.value)
+
+    def evict_lru(self, want_free: int, stream=None) -> int:
+        n = C.c_int32()
+        _call("halo_pool_evict_lru", self.handle, want_free, self._s(stream), C.byref(n))
+        return int(n.value)
 
     # ---- migration ----
     def comm_init(self, uid: bytes, nranks: int, rank: int):

@@ -363,6 +363,8 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
             }
             auto nit = p->nodes.find(id);
             if (nit == p->nodes.end()) return fail(HALO_EINVAL, "dangling node %lld", (long long)id);
+            if (nit->second.on_host)
+                return fail(HALO_EBUSY, "node %lld is offloaded to host memory: fetch it first", (long long)id);
             PNode pn;
             pn.id = id;
             pn.parent = -1;
@@ -376,6 +378,10 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
             id = nit->second.parent;
         }
     }
+    // LRU clock: every node this plan reads is "used now"
+    ++p->plan_tick;
+    for (auto &n : ns) const_cast<Node *>(n.node)->last_use = p->plan_tick;
+    pl->layout_gen = p->layout_gen;
     // deterministic child order: by node id
     std::vector<int> roots;
     {
@@ -764,6 +770,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
 halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, float *lse,
                       float scale, cudaStream_t s, int mask = 3) {
     halo_pool p = pl->pool;
+    if (pl->layout_gen != p->layout_gen)
+        return fail(HALO_EBUSY, "stale plan: a prefix node was offloaded or fetched since it was built");
     cudaError_t e;
     if (mask & 1) {
         e = launch_prefix_attn(&p->tmap_k, &p->tmap_v, &p->tmap_k8, &p->tmap_v8, pl->dev, p->geom, layer, q, scale, s);
@@ -801,6 +809,103 @@ std::vector<int32_t> token_slots(const std::vector<int32_t> &blocks, int64_t n) 
     std::vector<int32_t> slots(n);
     for (int64_t i = 0; i < n; ++i) slots[i] = blocks[i / kBlockTok] * kBlockTok + (int32_t)(i % kBlockTok);
     return slots;
+}
+
+// ---------------------------------------------------------------- host paging
+// Host blocks become reusable once the copies enqueued so far have passed (same scheme as
+// device blocks: events recorded on every stream that used the pool).
+void reclaim_host(halo_pool p, bool wait) {
+    for (size_t i = 0; i < p->host_pending.size();) {
+        PendingFree &pf = p->host_pending[i];
+        bool done = true;
+        for (cudaEvent_t e : pf.events) {
+            cudaError_t r = wait ? cudaEventSynchronize(e) : cudaEventQuery(e);
+            if (r == cudaErrorNotReady) {
+                done = false;
+                break;
+            }
+            if (r != cudaSuccess) cudaGetLastError();
+        }
+        if (!done) {
+            ++i;
+            continue;
+        }
+        for (auto it = pf.blocks.rbegin(); it != pf.blocks.rend(); ++it) p->host_free.push_back(*it);
+        for (cudaEvent_t e : pf.events) p->event_cache.push_back(e);
+        p->host_pending.erase(p->host_pending.begin() + i);
+    }
+}
+
+halo_status alloc_host_blocks(halo_pool p, int64_t n, std::vector<int32_t> &out) {
+    if ((int64_t)p->host_free.size() < n) reclaim_host(p, false);
+    if ((int64_t)p->host_free.size() < n) reclaim_host(p, true);
+    if ((int64_t)p->host_free.size() < n)
+        return fail(HALO_ENOMEM, "host arena out of blocks: need %lld, free %lld", (long long)n,
+                    (long long)p->host_free.size());
+    for (int64_t i = 0; i < n; ++i) {
+        out.push_back(p->host_free.back());
+        p->host_free.pop_back();
+    }
+    return HALO_OK;
+}
+
+void release_host_blocks(halo_pool p, std::vector<int32_t> &&blocks) {
+    if (blocks.empty()) return;
+    if (p->host_only) {
+        for (auto it = blocks.rbegin(); it != blocks.rend(); ++it) p->host_free.push_back(*it);
+        return;
+    }
+    PendingFree pf;
+    pf.blocks = std::move(blocks);
+    for (auto &f : p->streams) {
+        cudaEvent_t e = get_event(p);
+        if (e && cudaEventRecord(e, f.stream) == cudaSuccess) pf.events.push_back(e);
+        else cudaGetLastError();
+    }
+    p->host_pending.push_back(std::move(pf));
+}
+
+// Copy every layer of block list `dev` <-> `host` (same length), K and V, one cudaMemcpyAsync
+// per run of blocks consecutive on both sides (a registered node is one run per layer).
+halo_status copy_node_blocks(halo_pool p, const std::vector<int32_t> &dev, const std::vector<int32_t> &host,
+                             bool to_host, cudaStream_t s) {
+    const size_t bb = (size_t)p->cfg.num_kv_heads * kBlockTok * p->cfg.head_dim * 2;  // bytes per block per layer
+    const size_t dl = (size_t)p->cfg.capacity_blocks * bb, hl = (size_t)p->host_cap * bb;
+    for (int l = 0; l < p->cfg.num_layers; ++l) {
+        for (size_t i = 0; i < dev.size();) {
+            size_t j = i + 1;
+            while (j < dev.size() && dev[j] == dev[j - 1] + 1 && host[j] == host[j - 1] + 1) ++j;
+            const size_t n = (j - i) * bb;
+            for (int kv = 0; kv < 2; ++kv) {
+                uint8_t *d = static_cast<uint8_t *>(kv ? p->v : p->k) + l * dl + (size_t)dev[i] * bb;
+                uint8_t *h = static_cast<uint8_t *>(kv ? p->hv : p->hk) + l * hl + (size_t)host[i] * bb;
+                HALO_CUDA(cudaMemcpyAsync(to_host ? (void *)h : (void *)d, to_host ? (const void *)d : (const void *)h,
+                                          n, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, s));
+            }
+            i = j;
+        }
+    }
+    return HALO_OK;
+}
+
+halo_status offload_node(halo_pool p, Node &n, cudaStream_t s) {
+    std::vector<int32_t> hb;
+    halo_status st = alloc_host_blocks(p, (int64_t)n.blocks.size(), hb);
+    if (st != HALO_OK) return st;
+    if (!p->host_only) {
+        st = copy_node_blocks(p, n.blocks, hb, true, s);
+        if (st != HALO_OK) {
+            for (auto it = hb.rbegin(); it != hb.rend(); ++it) p->host_free.push_back(*it);
+            return st;
+        }
+        note_stream(p, s);
+    }
+    release_blocks(p, std::move(n.blocks));  // device blocks return once the copy has passed
+    n.blocks.clear();
+    n.host_blocks = std::move(hb);
+    n.on_host = true;
+    p->layout_gen++;
+    return HALO_OK;
 }
 
 }  // namespace
@@ -908,6 +1013,10 @@ halo_status halo_pool_destroy(halo_pool p) {
         if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
         if (p->side) cudaStreamDestroy(p->side);
         if (p->mig_buf) cudaFree(p->mig_buf);
+        for (auto &pf : p->host_pending)
+            for (cudaEvent_t e : pf.events) cudaEventDestroy(e);
+        if (p->hk) cudaFreeHost(p->hk);
+        if (p->hv) cudaFreeHost(p->hv);
         if (p->own_storage) {
             cudaFree(p->k);
             cudaFree(p->v);
@@ -993,6 +1102,7 @@ halo_status halo_prefix_release(halo_pool p, int64_t node) {
     DeviceGuard dg(p);
     const int64_t parent = it->second.parent;
     release_blocks(p, std::move(it->second.blocks));
+    release_host_blocks(p, std::move(it->second.host_blocks));
     p->nodes.erase(it);
     if (parent >= 0) p->nodes[parent].children--;
     return HALO_OK;
@@ -1005,6 +1115,7 @@ halo_status halo_prefix_read(halo_pool p, int64_t node, void *k_out, void *v_out
     if (p->host_only) return fail(HALO_EUNSUPPORTED, "host-only pool");
     auto it = p->nodes.find(node);
     if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (it->second.on_host) return fail(HALO_EBUSY, "node %lld is offloaded: fetch it first", (long long)node);
     if (!k_out || !v_out) return fail(HALO_EINVAL, "null output");
     DeviceGuard dg(p);
     cudaStream_t s = (cudaStream_t)stream;
@@ -1529,6 +1640,7 @@ halo_status halo_migrate_send(halo_pool p, int64_t node, int32_t dst_rank, int32
     if (!p->comm) return fail(HALO_ENCCL, "no communicator (halo_comm_init)");
     auto it = p->nodes.find(node);
     if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (it->second.on_host) return fail(HALO_EBUSY, "node %lld is offloaded: fetch it first", (long long)node);
     if (dst_rank < 0 || dst_rank >= p->nranks || dst_rank == p->rank) return fail(HALO_EINVAL, "bad destination rank");
     if (mode != 0 && mode != 1) return fail(HALO_EINVAL, "mode must be 0 (MOVE) or 1 (COPY)");
     if (mode == 0 && (it->second.children || it->second.requests))
@@ -1639,6 +1751,7 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
         return fail(HALO_EINVAL, "pools differ in device or KV geometry");
     auto it = src->nodes.find(node);
     if (it == src->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (it->second.on_host) return fail(HALO_EBUSY, "node %lld is offloaded: fetch it first", (long long)node);
     if (!node_out) return fail(HALO_EINVAL, "null node_out");
     if (parent_dst >= 0 && !dst->nodes.count(parent_dst))
         return fail(HALO_ENOENT, "unknown parent %lld", (long long)parent_dst);
@@ -1676,6 +1789,127 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
     dst->nodes.emplace(id, std::move(n));
     if (parent_dst >= 0) dst->nodes[parent_dst].children++;
     *node_out = id;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+// ---------------------------------------------------------------- host paging API
+halo_status halo_pool_host_reserve(halo_pool p, int64_t host_blocks) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (host_blocks < 0 || host_blocks * p->cfg.num_kv_heads > (int64_t)kBlkMask + 1 ||
+        (int64_t)p->cfg.num_layers * host_blocks >= ((int64_t)1 << 31))
+        return fail(HALO_EINVAL, "host_blocks out of range");
+    for (auto &n : p->nodes)
+        if (n.second.on_host) return fail(HALO_EBUSY, "nodes are offloaded to the current arena");
+    DeviceGuard dg(p);
+    if (!p->host_only) {
+        for (auto &pf : p->host_pending)
+            for (cudaEvent_t e : pf.events) cudaEventSynchronize(e);
+        if (p->hk) cudaFreeHost(p->hk);
+        if (p->hv) cudaFreeHost(p->hv);
+        p->hk = p->hv = nullptr;
+        const size_t bytes = (size_t)p->cfg.num_layers * host_blocks * p->cfg.num_kv_heads * kBlockTok *
+                             p->cfg.head_dim * 2;
+        if (bytes && (cudaHostAlloc(&p->hk, bytes, cudaHostAllocDefault) != cudaSuccess ||
+                      cudaHostAlloc(&p->hv, bytes, cudaHostAllocDefault) != cudaSuccess)) {
+            cudaGetLastError();
+            if (p->hk) cudaFreeHost(p->hk);
+            p->hk = p->hv = nullptr;
+            p->host_cap = 0;
+            p->host_free.clear();
+            return fail(HALO_ENOMEM, "pinned host arena of %zu bytes x 2", bytes);
+        }
+    }
+    for (auto &pf : p->host_pending) p->event_cache.insert(p->event_cache.end(), pf.events.begin(), pf.events.end());
+    p->host_pending.clear();
+    p->host_cap = host_blocks;
+    p->host_free.clear();
+    for (int64_t b = host_blocks - 1; b >= 0; --b) p->host_free.push_back((int32_t)b);
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_prefix_offload(halo_pool p, int64_t node, void *stream) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (it->second.on_host) return fail(HALO_EINVAL, "node %lld is already offloaded", (long long)node);
+    if (p->host_cap == 0) return fail(HALO_EUNSUPPORTED, "no host arena (halo_pool_host_reserve)");
+    DeviceGuard dg(p);
+    return offload_node(p, it->second, (cudaStream_t)stream);
+    HALO_GUARD_END
+}
+
+halo_status halo_prefix_fetch(halo_pool p, int64_t node, void *stream) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    Node &n = it->second;
+    if (!n.on_host) return fail(HALO_EINVAL, "node %lld is not offloaded", (long long)node);
+    DeviceGuard dg(p);
+    std::vector<int32_t> db;
+    halo_status st = alloc_blocks(p, (int64_t)n.host_blocks.size(), db);
+    if (st != HALO_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!p->host_only) {
+        st = copy_node_blocks(p, db, n.host_blocks, false, s);
+        if (st != HALO_OK) {
+            unalloc_blocks(p, db, 0);
+            return st;
+        }
+        note_stream(p, s);
+    }
+    release_host_blocks(p, std::move(n.host_blocks));  // reusable once the copy has passed
+    n.host_blocks.clear();
+    n.blocks = std::move(db);
+    n.on_host = false;
+    p->layout_gen++;
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_node_residency(halo_pool p, int64_t node, int32_t *on_device, uint64_t *last_use) {
+    if (check_pool(p)) return HALO_EINVAL;
+    auto it = p->nodes.find(node);
+    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
+    if (on_device) *on_device = it->second.on_host ? 0 : 1;
+    if (last_use) *last_use = it->second.last_use;
+    return HALO_OK;
+}
+
+halo_status halo_pool_evict_lru(halo_pool p, int64_t want_free, void *stream, int32_t *n_evicted) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (p->host_cap == 0) return fail(HALO_EUNSUPPORTED, "no host arena (halo_pool_host_reserve)");
+    DeviceGuard dg(p);
+    auto free_now = [&]() {
+        int64_t f = (int64_t)p->free_list.size();
+        for (auto &pf : p->pending) f += (int64_t)pf.blocks.size();
+        return f;
+    };
+    // candidates: device-resident nodes not read by the latest plan, least recently used
+    // first (ties: lower id)
+    std::vector<std::pair<uint64_t, int64_t>> cand;
+    for (auto &n : p->nodes)
+        if (!n.second.on_host && !n.second.blocks.empty() && n.second.last_use < p->plan_tick)
+            cand.push_back({n.second.last_use, n.first});
+    std::sort(cand.begin(), cand.end());
+    int32_t ev = 0;
+    for (auto &c : cand) {
+        if (free_now() >= want_free) break;
+        Node &n = p->nodes[c.second];
+        if ((int64_t)p->host_free.size() < (int64_t)n.blocks.size()) reclaim_host(p, false);
+        if ((int64_t)p->host_free.size() < (int64_t)n.blocks.size()) break;  // arena full
+        halo_status st = offload_node(p, n, (cudaStream_t)stream);
+        if (st != HALO_OK) return st;
+        ++ev;
+    }
+    if (n_evicted) *n_evicted = ev;
+    if (free_now() < want_free)
+        return fail(HALO_ENOMEM, "could not free %lld blocks by eviction", (long long)want_free);
     return HALO_OK;
     HALO_GUARD_END
 }

@@ -19,9 +19,12 @@ namespace halo {
 struct Node {
     int64_t parent = -1;
     int32_t ntok = 0;
-    std::vector<int32_t> blocks;
+    std::vector<int32_t> blocks;       // device blocks (empty while offloaded)
     int32_t children = 0;
     int32_t requests = 0;
+    bool on_host = false;              // offloaded: KV lives in host_blocks of the host arena
+    std::vector<int32_t> host_blocks;
+    uint64_t last_use = 0;             // plan tick of the last plan that read the node (LRU)
 };
 
 struct Request {
@@ -107,6 +110,13 @@ struct halo_pool_s {
     std::unordered_map<int64_t, halo::Request> requests;
     int64_t next_id = 1;
     int32_t plans_alive = 0;
+    // host paging: pinned arena [layer][host block][head][16][d] x K, V
+    void *hk = nullptr, *hv = nullptr;
+    int64_t host_cap = 0;
+    std::vector<int32_t> host_free;
+    std::vector<halo::PendingFree> host_pending;
+    uint64_t plan_tick = 0;     // incremented per plan build (LRU clock)
+    uint64_t layout_gen = 0;    // incremented when a node's blocks move (offload / fetch)
     CUtensorMap tmap_k{}, tmap_v{};      // box: one 16-token block x 64 d
     CUtensorMap tmap_k8{}, tmap_v8{};    // box: 8 consecutive blocks (128 tokens) x 64 d
     // migration
@@ -131,6 +141,7 @@ struct halo_plan_s {
     std::vector<int32_t> chunk_info;  // [NC][4] K2 chunk bounds + unit range (PlanDev::chunk_info)
     std::vector<halo::PrefixTile> tiles;
     halo_plan_info info{};
+    uint64_t layout_gen = 0;    // pool layout generation the plan was built against
     std::vector<uint8_t> host_buf;   // host-only pools
     halo::PinRing pin_plan, pin_slots;
     void *dbuf = nullptr;

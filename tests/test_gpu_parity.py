@@ -325,3 +325,67 @@ def test_full_c3_analytics_sampled_at_bench_configuration():
     """C3 per GPU (BASELINE configs[3]): 8 templates x 8k-token contexts x 256 requests."""
     wl = make_config("analytics", layers=1)
     check(wl, layers=[0], sample=[0, 255, 256, 1100, 2047])
+
+
+def test_continuous_batching_requests_join_and_leave_between_steps():
+    """Continuous batching ("continuous batching ...
+    early stops and early joins"): requests under two templates join and finish between
+    decode steps; every step is one halo_decode_step over the active set (plan rebuilt in
+    place), and every active request's output equals the oracle over its own context:
+    prefix path + initial suffix + the tokens of the steps it took part in."""
+    wl = make_config("ragged_suffix", layers=2, nreq=48, prefix=300, lo=1, hi=90)
+    # two templates: re-parent half of the requests onto a second root node
+    from synth.workloads import NodeSpec, RequestSpec, Workload
+    nodes = [NodeSpec(0, -1, 300), NodeSpec(1, -1, 170)]
+    reqs = [RequestSpec(r.ident, r.ident % 2, r.suffix) for r in wl.requests]
+    wl = Workload("churn", 2, 32, 8, 128, nodes, reqs, wl.seed)
+    rng = np.random.Generator(np.random.PCG64(11))
+    join = rng.integers(0, 4, wl.nreq)             # step at which request r joins
+    leave = join + rng.integers(1, 5, wl.nreq)     # first step it no longer takes part in
+    pool = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, 4000, DEV)
+    node_ids = {}
+    for n in wl.nodes:
+        k, v = wl.node_kv(n.ident, "cuda")
+        node_ids[n.ident] = pool.register_prefix(-1, n.ntok, k, v)
+    rid, taken = {}, {r: [] for r in range(wl.nreq)}
+    plan = None
+    nsteps = int(leave.max())
+    for step in range(nsteps):
+        for r in range(wl.nreq):
+            if leave[r] == step and r in rid:
+                pool.close_request(rid.pop(r))
+            if join[r] == step:
+                rid[r] = pool.open_request(node_ids[wl.requests[r].leaf])
+                if wl.requests[r].suffix:
+                    kv = [wl.suffix_kv("cuda", layer=l, request=r) for l in range(wl.layers)]
+                    k = torch.stack([x[0] for x in kv]).contiguous()
+                    v = torch.stack([x[1] for x in kv]).contiguous()
+                    pool.append([rid[r]], [wl.requests[r].suffix], k, v)
+        active = sorted(rid)
+        if not active:
+            continue
+        nk, nv = wl.new_kv(step, "cuda")
+        q = wl.q(step, "cuda")
+        idx = torch.tensor(active, device="cuda")
+        out = torch.empty((wl.layers, len(active), wl.hq, wl.d), device="cuda")
+        lse = torch.empty((wl.layers, len(active), wl.hq), device="cuda")
+        plan = pool.decode_step([rid[r] for r in active], nk[:, idx].contiguous(), nv[:, idx].contiguous(),
+                                q[:, idx].contiguous(), out, lse, reuse=plan)
+        torch.cuda.synchronize()
+        for r in active:
+            taken[r].append(step)
+        o, l_ = out.cpu().numpy(), lse.cpu().numpy()
+        for layer in range(wl.layers):
+            for i, r in enumerate(active):
+                kb, vb = oracle.request_context(wl, r, layer, steps=0)
+                for s in taken[r]:
+                    k1, v1 = wl.new_kv(s, "cpu", layer, request=r)
+                    kb = np.concatenate([kb, oracle._bits(k1)[None]])
+                    vb = np.concatenate([vb, oracle._bits(v1)[None]])
+                qb = oracle._bits(wl.q(step, "cpu", layer, request=r))
+                ro, rl = oracle.attend(qb, kb, vb, 1.0 / np.sqrt(wl.d))
+                assert np.abs(o[layer, i] - ro).max() <= OUT_TOL, (step, layer, r)
+                assert np.abs(l_[layer, i] - rl).max() <= LSE_TOL, (step, layer, r)
+    if plan is not None:
+        plan.destroy()
+    pool.destroy()

@@ -404,6 +404,9 @@ def main():
     # ---- host paging of the template node (NEXT-2) ----
     if not args.no_migration and not args.profile:
         extra["paging"] = measure_paging(pool, ld, wl, torch)
+    # ---- continuous batching under churn (NEXT-3) ----
+    if not args.no_e2e and not args.profile:
+        extra["continuous"] = measure_continuous(halo, wl, dev, torch, min(args.steps, 30))
     # ---- per-launch rooflines on the other configs (C2, C3) ----
     if args.other_configs and not args.profile:
         extra["other_configs"] = measure_other_configs(
@@ -445,6 +448,50 @@ def main():
     pool.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_continuous(halo, wl, dev, torch, steps, churn=0.125):
+    """A serving loop on the C1 shape: each step `churn` of the 256 requests finish (closed)
+    and as many new ones join under the template (opened + their 255-token prompt suffix
+    appended), then one halo_decode_step over the batch (device-resident q / new K / V).
+    Requests stay at most 1/churn steps, so suffix lengths spread over [255, 255 + 1/churn].
+    Device time with CUDA events (host bookkeeping included in the stream gaps)."""
+    from paper_2509_02121_b200.loader import blocks_needed, load
+    L, R = wl.layers, wl.nreq
+    ld = load(wl, dev, capacity=blocks_needed(wl, steps=int(1 / churn) + 4, slack=8192))
+    pool = ld.pool
+    tmpl = ld.node_ids[0]
+    S = wl.requests[0].suffix
+    sk, sv = wl.suffix_kv(f"cuda:{dev}")                  # [L][R*S][Hkv][d]
+    sk = sk.view(L, R, S, wl.hkv, wl.d)[:, 0].contiguous()   # one prompt suffix, reused
+    sv = sv.view(L, R, S, wl.hkv, wl.d)[:, 0].contiguous()
+    nk, nv = wl.new_kv(0, f"cuda:{dev}")
+    q = wl.q(0, f"cuda:{dev}")
+    out = torch.empty((L, R, wl.hq, wl.d), device=f"cuda:{dev}")
+    reqs = list(ld.req_ids)
+    k_turn = max(1, int(R * churn))
+    plan = None
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for it in range(steps + 3):
+        if it == 3:
+            torch.cuda.synchronize()
+            e0.record(stream)
+        lo = (it * k_turn) % R
+        for j in range(lo, lo + k_turn):                  # finish k requests, admit k new ones
+            pool.close_request(reqs[j % R])
+            reqs[j % R] = pool.open_request(tmpl)
+        joined = [reqs[j % R] for j in range(lo, lo + k_turn)]
+        pool.append(joined, [S] * k_turn, sk.repeat(1, k_turn, 1, 1), sv.repeat(1, k_turn, 1, 1))
+        plan = pool.decode_step(reqs, nk, nv, q, out, reuse=plan)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    plan.destroy()
+    pool.destroy()
+    return {"what": f"C1 serving loop: {k_turn} of {R} requests finish and {k_turn} join per step "
+                    f"(prompt suffix {S} tokens appended on join), then halo_decode_step",
+            "steps": steps, "ms_per_step": ms, "value": R * L / (ms * 1e-3), "unit": UNIT}
 
 
 def measure_paging(pool, ld, wl, torch):

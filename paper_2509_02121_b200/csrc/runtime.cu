@@ -1522,11 +1522,18 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
     const uint16_t *dq = q_host ? static_cast<const uint16_t *>(pl->q_stage) : static_cast<const uint16_t *>(q);
     float *dout = o_host ? pl->o_stage : out;
     float *dlse = l_host ? pl->l_stage : lse;
+    if (!kv_host) {  // device-resident new K/V: one K5 launch appends every layer
+        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dv, nreq, pl->slot_stage, nreq, 0, 0, L,
+                                          p->num_sms, s);
+        if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
+    }
     for (int l = 0; l < L; ++l) {
         HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_in[l], 0));
-        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk + kv_layer * l, dv + kv_layer * l, nreq,
-                                          pl->slot_stage, nreq, 0, l, l + 1, p->num_sms, s);
-        if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
+        if (kv_host) {  // host K/V: append layer l once its copy has landed
+            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk + kv_layer * l, dv + kv_layer * l, nreq,
+                                              pl->slot_stage, nreq, 0, l, l + 1, p->num_sms, s);
+            if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
+        }
         st = run_layer(pl, l, dq + q_layer * l, dout + q_layer * l, dlse ? dlse + rows * l : nullptr, scale, s);
         if (st != HALO_OK) return st;
         HALO_CUDA(cudaEventRecord(pl->ev_out[l], s));

@@ -158,6 +158,18 @@ typedef struct {
  * (no prefix and no suffix token) are EINVAL. */
 halo_status halo_decode_plan(halo_pool pool, int32_t nreq, const int64_t *reqs,
                              const halo_plan_options *opt, void *stream, halo_plan *inout);
+/* Prefill against cached prefixes (PAPER.md:121 §2.1 prefill; :321 KV-cache reuse discount
+ * gamma; :343 shared prefix cache): request reqs[i] has just appended ntok[i] >= 1 prompt
+ * tokens (the last ntok[i] tokens of its suffix, K/V already in the pool via
+ * halo_suffix_append).  The plan's rows are those tokens, request by request in the given
+ * order, tokens in order (sum ntok rows); row t of request i attends to the request's prefix
+ * path and to its suffix up to and including that token (causal within the prompt).  Run it
+ * with halo_decode_run / halo_decode_layers with q / out / lse rows = the new tokens
+ * ([sum ntok][Hq][d]).  The shared-prefix part is K1 on tensor cores over all the tokens of
+ * all the requests under a node; the causal suffix part runs in K2 (each token streams the
+ * suffix blocks it sees).  EINVAL if ntok[i] is out of [1, suffix length]. */
+halo_status halo_prefill_plan(halo_pool pool, int32_t nreq, const int64_t *reqs, const int32_t *ntok,
+                              const halo_plan_options *opt, void *stream, halo_plan *inout);
 /* Attention of layer `layer` for the planned batch:
  *   q   : bf16 [nreq][num_q_heads][head_dim], rows in the order given to the plan
  *   out : fp32 [nreq][num_q_heads][head_dim]   normalised attention output

@@ -61,6 +61,7 @@ SIGNATURES = {
     "halo_decode_run": (_i32, [_p, _i32, _p, _p, _p, _f, _p]),
     "halo_decode_run_stages": (_i32, [_p, _i32, _i32, _p, _p, _p, _f, _p]),
     "halo_decode_layers": (_i32, [_p, _i32, _p, _p, _p, _f, _p]),
+    "halo_prefill_plan": (_i32, [_p, _i32, _pi64, _pi32, C.POINTER(PlanOptions), _p, C.POINTER(_p)]),
     "halo_decode_step": (_i32, [_p, _i32, _pi64, _p, _p, _p, _p, _p, _f, C.POINTER(PlanOptions), _p,
                                 C.POINTER(_p)]),
     "halo_plan_get_info": (_i32, [_p, C.POINTER(PlanInfo)]),
@@ -254,6 +255,18 @@ class Pool:
             reuse.nreq = len(reqs)
             return reuse
         return Plan(self, h, len(reqs))
+
+    def prefill_plan(self, reqs, ntok, options: PlanOptions | None = None, stream=None,
+                     reuse: "Plan" = None):
+        """halo_prefill_plan: rows = the last ntok[i] suffix tokens of each request (causal)."""
+        h = C.c_void_p(reuse.handle.value if reuse is not None else None)
+        _call("halo_prefill_plan", self.handle, len(reqs), _i64_array(reqs), _i32_array(ntok),
+              C.byref(options) if options is not None else None, self._s(stream), C.byref(h))
+        rows = int(sum(ntok))
+        if reuse is not None:
+            reuse.nreq = rows
+            return reuse
+        return Plan(self, h, rows)
 
     def decode_step(self, reqs, k_new, v_new, q, out, lse=None, scale: float = 0.0,
                     options: PlanOptions | None = None, stream=None, reuse: "Plan" = None):

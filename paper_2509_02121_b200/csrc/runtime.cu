@@ -329,7 +329,11 @@ int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_
     return best_c;
 }
 
-halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
+// `virt` (prefill): the plan's rows are these virtual requests -- one per new prompt token,
+// with its request's leaf and the prefix of its suffix blocks up to and including the token
+// -- instead of the pool requests `reqs`.
+halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
+                       const std::vector<Request> *virt = nullptr) {
     halo_pool p = pl->pool;
     const auto &cfg = p->cfg;
     const int g = cfg.num_q_heads / cfg.num_kv_heads;
@@ -340,6 +344,10 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs) {
     // 1. requests
     std::vector<const Request *> R(nreq);
     for (int i = 0; i < nreq; ++i) {
+        if (virt) {
+            R[i] = &(*virt)[i];
+            continue;
+        }
         auto it = p->requests.find(reqs[i]);
         if (it == p->requests.end())
             return fail(HALO_ENOENT, "unknown request id %lld", (long long)reqs[i]);
@@ -1319,6 +1327,65 @@ halo_status halo_decode_plan(halo_pool p, int32_t nreq, const int64_t *reqs, con
     pl->pool = p;
     pl->opt = opt ? *opt : halo_plan_options{};
     halo_status st = build_plan(pl, nreq, reqs);
+    if (st == HALO_OK) st = upload_plan(pl, (cudaStream_t)stream);
+    if (st != HALO_OK) {
+        if (fresh) {
+            if (pl->dbuf) cudaFree(pl->dbuf);
+            if (pl->part) cudaFree(pl->part);
+            if (pl->segbuf) cudaFree(pl->segbuf);
+            if (pl->counters) cudaFree(pl->counters);
+            pl->pin_plan.release();
+            delete pl;
+        }
+        return st;
+    }
+    if (fresh) {
+        p->plans_alive++;
+        *inout = pl;
+    }
+    note_stream(p, (cudaStream_t)stream);
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_prefill_plan(halo_pool p, int32_t nreq, const int64_t *reqs, const int32_t *ntok,
+                              const halo_plan_options *opt, void *stream, halo_plan *inout) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!inout || nreq < 1 || !reqs || !ntok) return fail(HALO_EINVAL, "need nreq >= 1, reqs, ntok and a plan slot");
+    if (*inout && (*inout)->pool != p) return fail(HALO_EINVAL, "plan belongs to another pool");
+    if (opt && (opt->force_splits < 0)) return fail(HALO_EINVAL, "bad plan options");
+    // one virtual request per new token: token t of request i sees the request's prefix path
+    // and the first (len - ntok[i] + t + 1) suffix tokens (causal within the prompt)
+    std::vector<Request> virt;
+    int64_t total = 0;
+    for (int i = 0; i < nreq; ++i) {
+        auto it = p->requests.find(reqs[i]);
+        if (it == p->requests.end()) return fail(HALO_ENOENT, "unknown request id %lld", (long long)reqs[i]);
+        const Request &r = it->second;
+        if (ntok[i] < 1 || ntok[i] > r.len)
+            return fail(HALO_EINVAL, "request %lld: %d new tokens but a %d-token suffix", (long long)reqs[i],
+                        ntok[i], r.len);
+        total += ntok[i];
+        if (total > INT32_MAX / 64) return fail(HALO_EINVAL, "too many prefill tokens");
+    }
+    virt.reserve(total);
+    for (int i = 0; i < nreq; ++i) {
+        const Request &r = p->requests[reqs[i]];
+        for (int32_t t = 0; t < ntok[i]; ++t) {
+            Request v;
+            v.leaf = r.leaf;
+            v.len = r.len - ntok[i] + t + 1;
+            v.blocks.assign(r.blocks.begin(), r.blocks.begin() + ceil_div(v.len, kBlockTok));
+            virt.push_back(std::move(v));
+        }
+    }
+    DeviceGuard dg(p);
+    const bool fresh = *inout == nullptr;
+    halo_plan pl = fresh ? new halo_plan_s() : *inout;
+    pl->pool = p;
+    pl->opt = opt ? *opt : halo_plan_options{};
+    halo_status st = build_plan(pl, (int32_t)total, nullptr, &virt);
     if (st == HALO_OK) st = upload_plan(pl, (cudaStream_t)stream);
     if (st != HALO_OK) {
         if (fresh) {

@@ -389,3 +389,46 @@ def test_continuous_batching_requests_join_and_leave_between_steps():
     if plan is not None:
         plan.destroy()
     pool.destroy()
+
+
+@pytest.mark.parametrize("min_rows", [0, 1, 100000])
+def test_prefill_against_cached_prefixes_matches_oracle(min_rows):
+    """halo_prefill_plan (NEXT-4): a burst of prompt tokens per request attends causally to
+    itself after the cached prefix path; every token row vs the oracle over its context."""
+    wl = make_config("ragged", layers=2)
+    ld = load(wl, DEV)
+    rng = np.random.Generator(np.random.PCG64(3))
+    sel = [i for i in range(wl.nreq) if i % 3 == 0]
+    nnew = [int(x) for x in rng.integers(1, 40, len(sel))]
+    # the prompt tokens of request r are the decode-step tokens 0..n-1 of the workload
+    nkv = [wl.new_kv(s, "cuda") for s in range(max(nnew))]      # [L][R][Hkv][d] per step
+    qs = [wl.q(s, "cuda") for s in range(max(nnew))]
+    ks, vs = [], []
+    for r, n in zip(sel, nnew):
+        ks.append(torch.stack([nkv[s][0][:, r] for s in range(n)], dim=1))
+        vs.append(torch.stack([nkv[s][1][:, r] for s in range(n)], dim=1))
+    ld.pool.append([ld.req_ids[r] for r in sel], nnew, torch.cat(ks, 1).contiguous(), torch.cat(vs, 1).contiguous())
+    plan = ld.pool.prefill_plan([ld.req_ids[r] for r in sel], nnew, opts(min_rows=min_rows))
+    rows = sum(nnew)
+    qrows = torch.cat([torch.stack([qs[s][:, r] for s in range(n)], dim=1)
+                       for r, n in zip(sel, nnew)], 1).contiguous()      # [L][rows][Hq][d]
+    out = torch.empty((wl.layers, rows, wl.hq, wl.d), device="cuda")
+    lse = torch.empty((wl.layers, rows, wl.hq), device="cuda")
+    for layer in range(wl.layers):
+        plan.run(layer, qrows[layer], out[layer], lse[layer])
+    torch.cuda.synchronize()
+    o, l_ = out.cpu().numpy(), lse.cpu().numpy()
+    for layer in range(wl.layers):
+        row = 0
+        for r, n in zip(sel, nnew):
+            kb, vb = oracle.request_context(wl, r, layer, steps=0)
+            for t in range(n):
+                k1, v1 = wl.new_kv(t, "cpu", layer, request=r)
+                kb = np.concatenate([kb, oracle._bits(k1)[None]])
+                vb = np.concatenate([vb, oracle._bits(v1)[None]])
+                qb = oracle._bits(wl.q(t, "cpu", layer, request=r))
+                ro, rl = oracle.attend(qb, kb, vb, 1.0 / np.sqrt(wl.d))
+                assert np.abs(o[layer, row] - ro).max() <= OUT_TOL, (layer, r, t)
+                assert np.abs(l_[layer, row] - rl).max() <= LSE_TOL, (layer, r, t)
+                row += 1
+    cleanup(ld, plan)

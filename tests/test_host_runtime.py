@@ -242,3 +242,28 @@ def test_k2_chunk_schedule_covers_every_block_once(cfg, kw, cb):
         assert visits[u] == list(range(visits[u][0], visits[u][0] + nseg[u]))
     pl.destroy()
     p.destroy()
+
+
+def test_prefill_plan_rows_are_causal_virtual_requests():
+    """halo_prefill_plan (NEXT-4): one row per new prompt token; token t of request i sees
+    the first len - ntok + t + 1 suffix tokens (its K2 block list grows with t)."""
+    p = host_pool(layers=1, hkv=2, hq=8, cap=400)
+    a = p.register_prefix(-1, 100)
+    r1, r2 = p.open_request(a), p.open_request(-1)
+    p.append([r1, r2], [20, 40])
+    pl = p.prefill_plan([r1, r2], [20, 33])
+    info = pl.info()
+    assert info["nreq"] == 53
+    off = pl.export("req_blk_off")
+    nblk = np.diff(off)
+    # r1 rows: suffix lengths 1..20; r2 rows: 8..40 (no prefix: the whole context is K2's)
+    want = [(n + 15) // 16 for n in range(1, 21)] + [(n + 15) // 16 for n in range(8, 41)]
+    if info["tensor_nodes"] == 0:       # prefix folded into K2: +7 blocks for r1's rows
+        want = [w + 7 for w in want[:20]] + want[20:]
+    assert list(nblk) == want
+    pl.destroy()
+    for bad in ([0, 1], [21, 1], [1, 41]):
+        with pytest.raises(halo.HaloError) as e:
+            p.prefill_plan([r1, r2], bad)
+        assert e.value.name == "HALO_EINVAL"
+    p.destroy()

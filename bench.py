@@ -407,6 +407,9 @@ def main():
     # ---- continuous batching under churn (NEXT-3) ----
     if not args.no_e2e and not args.profile:
         extra["continuous"] = measure_continuous(halo, wl, dev, torch, min(args.steps, 30))
+    # ---- shared-prefix prefill (NEXT-4) ----
+    if not args.no_e2e and not args.profile:
+        extra["prefill"] = measure_prefill(halo, dev, torch, steps=min(args.steps, 10))
     # ---- per-launch rooflines on the other configs (C2, C3) ----
     if args.other_configs and not args.profile:
         extra["other_configs"] = measure_other_configs(
@@ -448,6 +451,53 @@ def main():
     pool.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_prefill(halo, dev, torch, steps=10, prompt=64, layers=4):
+    """Prefill of a `prompt`-token task prompt for each of the 256 C1 requests against the
+    cached 2048-token template (halo_prefill_plan + halo_decode_run per layer): 16,384 query
+    rows per kv head through K1 (tensor cores over the shared prefix) and the causal prompt
+    part in K2.  Per-kernel CUDA events; `layers` layers (per-layer work of the full model)."""
+    from paper_2509_02121_b200.loader import blocks_needed, load
+    from synth import make_config
+    wl = make_config("fanout", layers=layers, suffix=0)
+    R, L = wl.nreq, wl.layers
+    ld = load(wl, dev, capacity=blocks_needed(wl, steps=prompt + 2, slack=4096))
+    pool = ld.pool
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(7)
+    k = (torch.randn((L, R * prompt, wl.hkv, wl.d), device=f"cuda:{dev}", generator=g)).bfloat16()
+    v = (torch.randn((L, R * prompt, wl.hkv, wl.d), device=f"cuda:{dev}", generator=g)).bfloat16()
+    q = (torch.randn((L, R * prompt, wl.hq, wl.d), device=f"cuda:{dev}", generator=g)).bfloat16()
+    out = torch.empty((L, R * prompt, wl.hq, wl.d), device=f"cuda:{dev}")
+    pool.append(ld.req_ids, [prompt] * R, k, v)
+    plan = pool.prefill_plan(ld.req_ids, [prompt] * R)
+    info = plan.info()
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps * L)]
+    for _ in range(2):
+        for l in range(L):
+            plan.run(l, q[l], out[l])
+    torch.cuda.synchronize()
+    i = 0
+    for _ in range(steps):
+        for l in range(L):
+            ev[i][0].record(stream)
+            plan.run_stages(l, 1, q[l], out[l])
+            ev[i][1].record(stream)
+            plan.run_stages(l, 2, q[l], out[l])
+            ev[i][2].record(stream)
+            i += 1
+    torch.cuda.synchronize()
+    n = steps * L
+    k1 = sum(e[0].elapsed_time(e[1]) for e in ev) / n
+    k2 = sum(e[1].elapsed_time(e[2]) for e in ev) / n
+    k2r, k1r = kernel_rooflines(info, k1, k2)
+    plan.destroy()
+    pool.destroy()
+    return {"what": f"prefill of a {prompt}-token prompt for each of {R} requests against the cached "
+                    f"{wl.nodes[0].ntok}-token template (rows = {R * prompt} tokens x {wl.hq} q-heads)",
+            "layer_ms": k1 + k2, "tokens_per_s": R * prompt / ((k1 + k2) * 1e-3),
+            "prefix_roofline": k1r, "suffix_roofline": k2r, "k1_tiles": info["k1_tiles"]}
 
 
 def measure_continuous(halo, wl, dev, torch, steps, churn=0.125):

@@ -11,14 +11,11 @@ constexpr int kBlockTok = 16;       // tokens per KV block
 constexpr int kK1Rows = 256;        // K1 tile rows (two UMMA M=128 sub-tiles)
 constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
 constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N above this; bounded by smem)
-#ifndef HALO_K2_WARPS
-#define HALO_K2_WARPS 12
-#endif
-#ifndef HALO_K2_STAGES
-#define HALO_K2_STAGES 2
-#endif
-constexpr int kK2Warps = HALO_K2_WARPS;    // K2 warps per CTA (one CTA per SM)
-constexpr int kK2Stages = HALO_K2_STAGES;  // K2 smem ring stages per warp (16-token K+V blocks)
+// K2 launch shapes (one CTA per SM): "wide" = 12 warps x 2 ring stages (many units per warp:
+// best latency hiding), "narrow" = 7 warps x 4 stages (chosen by the planner when units are
+// few per warp and whole units divide evenly over 7 warps per SM: no stream-K pieces).
+constexpr int kK2WarpsWide = 12, kK2StagesWide = 2;
+constexpr int kK2WarpsNarrow = 7, kK2StagesNarrow = 4;
 constexpr int kBlkCountShift = 27;  // K2 block entry: block | (ntok-1) << 27 (| unit start << 31)
 constexpr uint32_t kBlkMask = (1u << kBlkCountShift) - 1;
 
@@ -70,6 +67,7 @@ struct PlanDev {
     float *seg_o;                // [nseg_total][g][D]  unnormalised o (base-2 state)
     float *seg_ml;               // [nseg_total][g][2]  (m, l)
     int32_t ntiles, nreq, nunits, max_slots, nwarps, nchunks, nblocks;
+    int32_t k2_warps;            // K2 warps per CTA: kK2WarpsWide or kK2WarpsNarrow
 };
 
 struct PoolGeom {

@@ -10,10 +10,10 @@
 //
 // B200 design:
 //  * static schedule: the (request, kv head) units' blocks form one sequence, cut by the
-//    planner into equal contiguous chunks, one per warp (148 SMs x kK2Warps).  A unit cut
+//    planner into equal contiguous chunks, one per warp (148 SMs x 12 or 7 warps).  A unit cut
 //    by chunk boundaries leaves one partial softmax state per piece; the last piece to
 //    finish (atomic arrival counter) merges them in a fixed order -> bit-deterministic.
-//  * warp-level streaming: every warp owns a ring of kK2Stages smem stages; its lane 0
+//  * warp-level streaming: every warp owns a ring of 2 (or 4) smem stages; its lane 0
 //    issues one 1-D bulk async copy (cp.async.bulk, TMA engine) per 4-KiB K slab and V
 //    slab of a 16-token block, completion on a per-stage mbarrier.  The unit's g query
 //    rows (contiguous, g*d*2 bytes) arrive the same way, double-buffered, so neither a
@@ -41,8 +41,6 @@ namespace {
 #define HALO_K2_QK_BF16 0  // 1: q.k with mixed-precision bf16 FMAs (no K conversion, q kept as bf16)
 #endif
 
-constexpr int kWarps = kK2Warps;
-constexpr int kStages = kK2Stages;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLazy = 8.f;  // base-2 headroom of the lazy running max (p <= 2^8)
@@ -59,13 +57,12 @@ struct SuffixArgs {
 
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
-template <int D, int G>
+template <int D, int G, int kWarps, int kStages>
 struct Shape {
     static constexpr int LPT = cmax(2, cmax(G, G * D / 64));  // lanes per token row
     static constexpr int TPI = 32 / LPT;                      // tokens per warp iteration
     static constexpr int NIT = kBlockTok / TPI;
     static constexpr int NCH = D / (8 * LPT);                 // 16-B chunks per lane per row (q.k)
-    static constexpr int DPL = D / 32;                        // output dims per lane (P.V)
     static constexpr int SLAB = kBlockTok * D * 2;            // bytes of one (block, head) slab
     static constexpr int STAGE = 2 * SLAB;                    // K + V
     static constexpr int QB = G * D * 2;                      // the unit's q rows (bf16)
@@ -111,7 +108,7 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[G], int c) {
 }
 
 template <int D, int G>
-using QAcc = float2[G][Shape<D, G>::NCH][4];  // q.k mapping: G heads x this lane's row chunks
+using QAcc = float2[G][Shape<D, G, 1, 2>::NCH][4];  // q.k mapping: G heads x this lane's row chunks
 template <int D, int G>
 using OAcc = float2[G][D / 64];               // P.V mapping: G heads x this lane's D/32 dims
 
@@ -190,9 +187,9 @@ __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head,
     }
 }
 
-template <int D, int G>
+template <int D, int G, int kWarps, int kStages>
 __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const SuffixArgs a) {
-    using S = Shape<D, G>;
+    using S = Shape<D, G, kWarps, kStages>;
     constexpr int LPT = S::LPT, TPI = S::TPI, NIT = S::NIT, NCH = S::NCH, ST = S::ST;
     constexpr int NP = D / 64, DPL = D / 32;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -550,11 +547,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     }
 }
 
-template <int D, int G>
+template <int D, int G, int kWarps, int kStages>
 cudaError_t launch_t(const SuffixArgs &a, cudaStream_t s) {
-    using S = Shape<D, G>;
+    using S = Shape<D, G, kWarps, kStages>;
     const int smem = kWarps * S::WARP_SMEM_AL;
-    auto kern = suffix_decode_kernel<D, G>;
+    auto kern = suffix_decode_kernel<D, G, kWarps, kStages>;
     int dev = 0;
     cudaGetDevice(&dev);
     static bool configured[64] = {};  // the attribute is per function and device
@@ -597,8 +594,10 @@ cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void
     a.hq = g.hq;
     a.qscale = scale * kLog2e;
     const int G = g.hq / g.hkv;
-#define HALO_K2_CASE(DD, GG) \
-    if (g.d == DD && G == GG) return launch_t<DD, GG>(a, s);
+#define HALO_K2_CASE(DD, GG)                                                                       \
+    if (g.d == DD && G == GG)                                                                      \
+        return p.k2_warps == kK2WarpsNarrow ? launch_t<DD, GG, kK2WarpsNarrow, kK2StagesNarrow>(a, s) \
+                                            : launch_t<DD, GG, kK2WarpsWide, kK2StagesWide>(a, s);
     HALO_K2_CASE(128, 1) HALO_K2_CASE(128, 2) HALO_K2_CASE(128, 4) HALO_K2_CASE(128, 8)
     HALO_K2_CASE(64, 1) HALO_K2_CASE(64, 2) HALO_K2_CASE(64, 4) HALO_K2_CASE(64, 8)
 #undef HALO_K2_CASE

@@ -547,7 +547,8 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     // 12b. K2 schedule: static chunks, warp w takes chunks w, w + W, ...
     {
         const int U = nreq * hkv;
-        const int64_t W = (int64_t)p->num_sms * kK2Warps;
+        int64_t W = (int64_t)p->num_sms * kK2WarpsWide;
+        pl->k2_warps = kK2WarpsWide;
         pl->unit_boff.assign(U + 1, 0);
         for (int u = 0; u < U; ++u) {
             const int req = pl->unit_req[u / hkv];
@@ -556,12 +557,36 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         const int64_t Btot = pl->unit_boff[U];
         std::vector<int32_t> &lo = pl->chunk_lo;
         lo.assign(1, 0);
+        // Cuts snapped to the nearest unit boundary, if the largest chunk stays within 5% of
+        // the equal share: whole units need no stream-K merge.
+        auto snap = [&](int64_t nw, std::vector<int32_t> &out) {
+            out.assign(1, 0);
+            size_t u = 0;
+            for (int64_t w = 1; w < nw; ++w) {
+                const int64_t b = w * Btot / nw;
+                while (u + 1 < pl->unit_boff.size() && pl->unit_boff[u + 1] <= b) ++u;
+                int64_t c = pl->unit_boff[u];
+                if (u + 1 < pl->unit_boff.size() && pl->unit_boff[u + 1] - b < b - c) c = pl->unit_boff[u + 1];
+                if (c > out.back() && c < Btot) out.push_back((int32_t)c);
+            }
+            int64_t mx = Btot - out.back();
+            for (size_t i = 1; i < out.size(); ++i) mx = std::max<int64_t>(mx, out[i] - out[i - 1]);
+            return mx * 100 <= ceil_div(Btot, nw) * 105;
+        };
+        std::vector<int32_t> cuts;
         if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
             for (int64_t x = pl->opt.k2_chunk_blocks; x < Btot; x += pl->opt.k2_chunk_blocks) lo.push_back((int32_t)x);
+        } else if (U < 2 * W && snap((int64_t)p->num_sms * kK2WarpsNarrow, cuts)) {
+            // few units per warp (stream-K pieces would dominate) and whole units divide
+            // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
+            pl->k2_warps = kK2WarpsNarrow;
+            W = (int64_t)p->num_sms * kK2WarpsNarrow;
+            lo = cuts;
+        } else if (snap(W, cuts)) {
+            lo = cuts;
         } else {
-            // static equal-bytes partition: warp w gets [w*Btot/W, (w+1)*Btot/W).  Measured
-            // alternatives (snapping cuts to unit ends: uneven chunks; a dynamic tail of small
-            // chunks: per-chunk setup latencies) were slower on B200.
+            // static equal-bytes partition: warp w gets [w*Btot/W, (w+1)*Btot/W).  (A dynamic
+            // tail of small chunks was slower: per-chunk setup latencies.)
             for (int64_t w = 1; w < W; ++w) {
                 const int64_t b = w * Btot / W;
                 if (b > lo.back() && b < Btot) lo.push_back((int32_t)b);
@@ -767,7 +792,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
     dv.seg_o = pl->segbuf;
     dv.seg_ml = pl->segbuf + (size_t)pl->nseg_total * gq * p->cfg.head_dim;
-    dv.nwarps = p->num_sms * kK2Warps;
+    dv.nwarps = p->num_sms * pl->k2_warps;
+    dv.k2_warps = pl->k2_warps;
     dv.ntiles = (int32_t)pl->tiles.size();
     dv.nreq = nreq;
     dv.nunits = nreq * p->cfg.num_kv_heads;

@@ -3,8 +3,8 @@
 set -x
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --profile --steps 2 --warmup 3 --other-configs "" > gpurun_out/launches.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"prefix_attn|suffix_decode|kv_" --csv --log-file gpurun_out/launches.csv \
+    python bench.py --profile --steps 3 --warmup 3 --other-configs "" > gpurun_out/launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:suffix_decode -s 40 -c 1 -o gpurun_out/k2full -f \
     python bench.py --profile --steps 2 --warmup 3 --other-configs "" > gpurun_out/k2full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:prefix_attn -s 40 -c 1 -o gpurun_out/k1full -f \

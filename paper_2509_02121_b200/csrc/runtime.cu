@@ -329,6 +329,15 @@ int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_
     return best_c;
 }
 
+// Test hook (HALO_K2_FORCE_NARROW=1): always use K2's narrow launch shape.
+bool force_narrow() {
+    static const bool f = [] {
+        const char *e = getenv("HALO_K2_FORCE_NARROW");
+        return e && atoi(e) != 0;
+    }();
+    return f;
+}
+
 // `virt` (prefill): the plan's rows are these virtual requests -- one per new prompt token,
 // with its request's leaf and the prefix of its suffix blocks up to and including the token
 // -- instead of the pool requests `reqs`.
@@ -576,7 +585,15 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         std::vector<int32_t> cuts;
         if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
             for (int64_t x = pl->opt.k2_chunk_blocks; x < Btot; x += pl->opt.k2_chunk_blocks) lo.push_back((int32_t)x);
-        } else if (U < 2 * W && snap((int64_t)p->num_sms * kK2WarpsNarrow, cuts)) {
+        } else if (force_narrow() || (U < 2 * W && snap((int64_t)p->num_sms * kK2WarpsNarrow, cuts))) {
+            if (force_narrow()) {  // test hook: equal cuts over the narrow shape
+                cuts.assign(1, 0);
+                const int64_t Wn = (int64_t)p->num_sms * kK2WarpsNarrow;
+                for (int64_t w = 1; w < Wn; ++w) {
+                    const int64_t b = w * Btot / Wn;
+                    if (b > cuts.back() && b < Btot) cuts.push_back((int32_t)b);
+                }
+            }
             // few units per warp (stream-K pieces would dominate) and whole units divide
             // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
             pl->k2_warps = kK2WarpsNarrow;

@@ -432,3 +432,27 @@ def test_prefill_against_cached_prefixes_matches_oracle(min_rows):
                 assert np.abs(l_[layer, row] - rl).max() <= LSE_TOL, (layer, r, t)
                 row += 1
     cleanup(ld, plan)
+
+
+def test_k2_narrow_launch_shape_on_every_head_layout():
+    """The planner picks K2's narrow shape (7 warps x 4 stages) only for C1-like batches;
+    force it (HALO_K2_FORCE_NARROW, read once per process: run in a subprocess) on ragged
+    trees, d=64/128 and g=1/2/4/8, stream-K pieces included."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import test_gpu_parity as t\n"
+        "from synth import make_config\n"
+        "t.halo_build.build(); t.halo.load_library(); t.torch.cuda.set_device(0)\n"
+        "t.check(make_config('ragged'), t.opts(min_rows=16))\n"
+        "t.check(make_config('ragged_suffix', layers=1, nreq=40, prefix=300, lo=1, hi=300))\n"
+        "t.check(make_config('fanout', layers=1, nreq=40, prefix=260, suffix=9, hq=16, hkv=2))\n"
+        "t.check(make_config('fanout', layers=1, nreq=70, prefix=333, suffix=17, hq=4, hkv=2, d=64))\n"
+        "t.check(make_config('fanout', layers=1, nreq=130, prefix=260, suffix=9, hq=4, hkv=4), t.opts(min_rows=1))\n"
+        "print('narrow ok')\n") % (os.path.dirname(os.path.abspath(__file__)),
+                                     os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, HALO_K2_FORCE_NARROW="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "narrow ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

@@ -36,6 +36,9 @@ static_assert(sizeof(PrefixTile) == 32, "PrefixTile is exported as int32 x 8");
 // Device view of a plan (all pointers into one device buffer).
 struct PlanDev {
     const PrefixTile *tiles;
+    const int4 *tile_aux;        // [ntiles] {caller index of the tile's first request if its
+                                 //  requests are consecutive else -1, pool block of its first
+                                 //  token if its blocks are consecutive else -1, -, -}
     const int32_t *req_order;    // caller indices, DFS order
     const int32_t *node_blocks;  // block ids of K1 nodes
     const int32_t *unit_req;     // K2 request order (caller indices, LPT)

@@ -126,6 +126,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     // griddepcontrol.wait) start on SMs this grid leaves idle and as its CTAs retire
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const PrefixTile T = a.p.tiles[blockIdx.x];
+    const int4 aux = a.p.tile_aux[blockIdx.x];  // loaded alongside T (no dependency)
     const int NT = (T.tok_end - T.tok_begin + kK1Tok - 1) / kK1Tok;
     const bool hasB = T.nrows > kSubRows;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -165,7 +166,11 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         int32_t *blocks = reinterpret_cast<int32_t *>(sm + C::OFF_BLK);
         const int blk_first = T.tok_begin / kBlockTok;
         const int nblk = (T.tok_end + kBlockTok - 1) / kBlockTok - blk_first;
-        for (int i = lane; i < nblk; i += 32) blocks[i] = a.p.node_blocks[T.blk_off + blk_first + i];
+        if (aux.y >= 0) {  // consecutive blocks: ids follow from the first (no global load)
+            for (int i = lane; i < nblk; i += 32) blocks[i] = aux.y + i;
+        } else {
+            for (int i = lane; i < nblk; i += 32) blocks[i] = a.p.node_blocks[T.blk_off + blk_first + i];
+        }
         __syncwarp();
         // PDL: this grid may start while the previous kernel drains; the pool blocks it reads
         // may have been written by that kernel (a registration or append), so wait here
@@ -301,7 +306,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         const uint32_t lane_addr = tmem + ((uint32_t)(32 * wq) << 16);
         const bool valid_row = trow < T.nrows;
         const int g = a.g;
-        const int req = valid_row ? a.p.req_order[T.req_off + trow / g] : 0;
+        const int req = !valid_row ? 0 : aux.x >= 0 ? aux.x + trow / g : a.p.req_order[T.req_off + trow / g];
         const int head = T.kv_head * g + trow % g;
         // Q row -> smem, K-major SW128 (16-B chunk c of row r lands at chunk c ^ (r & 7)).
         // q and the partials (read by the previous layer's K2) belong to earlier kernels.

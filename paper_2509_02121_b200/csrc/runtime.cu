@@ -517,6 +517,22 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     std::stable_sort(pl->tiles.begin(), pl->tiles.end(), [](const PrefixTile &a, const PrefixTile &b) {
         return (a.tok_end - a.tok_begin) > (b.tok_end - b.tok_begin);
     });
+    // 10b. per-tile shortcuts that save K1 a dependent global load each: the caller index of
+    // the tile's first request when its requests are consecutive caller indices (q rows are
+    // then addressed directly), and the pool block of its first token when the node's blocks
+    // over the tile's range are physically consecutive (TMA coordinates computed, no block list)
+    pl->tile_aux.assign(pl->tiles.size() * 4, -1);
+    for (size_t ti = 0; ti < pl->tiles.size(); ++ti) {
+        const PrefixTile &t = pl->tiles[ti];
+        const int nr = (t.nrows + g - 1) / g;
+        bool rc = true;
+        for (int i = 1; i < nr && rc; ++i) rc = pl->req_order[t.req_off + i] == pl->req_order[t.req_off] + i;
+        if (rc) pl->tile_aux[4 * ti] = pl->req_order[t.req_off];
+        const int b0 = t.tok_begin / kBlockTok, b1 = (t.tok_end + kBlockTok - 1) / kBlockTok;
+        bool bc = true;
+        for (int b = b0 + 1; b < b1 && bc; ++b) bc = pl->node_blocks[t.blk_off + b] == pl->node_blocks[t.blk_off + b - 1] + 1;
+        if (bc) pl->tile_aux[4 * ti + 1] = pl->node_blocks[t.blk_off + b0];
+    }
     // 11. K2 per-request block lists: folded path nodes root -> leaf, then the suffix
     pl->req_blk_off.assign(nreq + 1, 0);
     pl->req_blk.clear();
@@ -708,6 +724,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const size_t o_ent = off; off = align16(off + pl->k2_ent.size() * 4);
     const size_t o_umeta = off; off = align16(off + pl->unit_meta.size() * 4);
     const size_t o_cinfo = off; off = align16(off + pl->chunk_info.size() * 4);
+    const size_t o_taux = off; off = align16(off + pl->tile_aux.size() * 4);
     const size_t total = off;
     uint8_t *h;
     if (p->host_only) {
@@ -735,6 +752,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     put(o_ent, pl->k2_ent.data(), pl->k2_ent.size() * 4);
     put(o_umeta, pl->unit_meta.data(), pl->unit_meta.size() * 4);
     put(o_cinfo, pl->chunk_info.data(), pl->chunk_info.size() * 4);
+    put(o_taux, pl->tile_aux.data(), pl->tile_aux.size() * 4);
     if (p->host_only) return HALO_OK;
 
     if (pl->dbuf_cap < total) {
@@ -804,6 +822,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     dv.k2_ent = reinterpret_cast<const uint2 *>(d + o_ent);
     dv.unit_meta = reinterpret_cast<const int4 *>(d + o_umeta);
     dv.chunk_info = reinterpret_cast<const int4 *>(d + o_cinfo);
+    dv.tile_aux = reinterpret_cast<const int4 *>(d + o_taux);
     dv.nchunks = NC;
     dv.nblocks = pl->unit_boff.empty() ? 0 : pl->unit_boff.back();
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;

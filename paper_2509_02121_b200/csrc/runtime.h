@@ -140,6 +140,7 @@ struct halo_plan_s {
     std::vector<uint32_t> k2_ent;     // [Btot][2] K2 block descriptors (PlanDev::k2_ent)
     std::vector<int32_t> unit_meta;   // [U][8] K2 unit metadata (PlanDev::unit_meta)
     std::vector<int32_t> chunk_info;  // [NC][4] K2 chunk bounds + unit range (PlanDev::chunk_info)
+    std::vector<int32_t> tile_aux;    // [ntiles][4] K1 shortcuts (PlanDev::tile_aux)
     std::vector<halo::PrefixTile> tiles;
     halo_plan_info info{};
     uint64_t layout_gen = 0;    // pool layout generation the plan was built against

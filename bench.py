@@ -398,23 +398,30 @@ def main():
                         "steps": e2e_steps, "how": "halo_decode_step (append one token per request + "
                         "plan + all layers; per-layer H2D/D2H on library copy streams overlapped "
                         "with the kernels) with pinned host buffers; wall clock after sync"}
+    def guarded(key, fn):
+        """The secondary legs must not cost the headline line: a failure is reported in place."""
+        try:
+            extra[key] = fn()
+        except Exception as e:  # noqa: BLE001
+            extra[key] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.synchronize()
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
-        extra["migration"] = measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist)
+        guarded("migration", lambda: measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist))
     # ---- host paging of the template node (NEXT-2) ----
     if not args.no_migration and not args.profile:
-        extra["paging"] = measure_paging(pool, ld, wl, torch)
+        guarded("paging", lambda: measure_paging(pool, ld, wl, torch))
     # ---- continuous batching under churn (NEXT-3) ----
     if not args.no_e2e and not args.profile:
-        extra["continuous"] = measure_continuous(halo, wl, dev, torch, min(args.steps, 30))
+        guarded("continuous", lambda: measure_continuous(halo, wl, dev, torch, min(args.steps, 30)))
     # ---- shared-prefix prefill (NEXT-4) ----
     if not args.no_e2e and not args.profile:
-        extra["prefill"] = measure_prefill(halo, dev, torch, steps=min(args.steps, 10))
+        guarded("prefill", lambda: measure_prefill(halo, dev, torch, steps=min(args.steps, 10)))
     # ---- per-launch rooflines on the other configs (C2, C3) ----
     if args.other_configs and not args.profile:
-        extra["other_configs"] = measure_other_configs(
+        guarded("other_configs", lambda: measure_other_configs(
             halo, [x for x in args.other_configs.split(",") if x], args.other_layers,
-            max(3, min(args.steps, 10)), 3, world, dev, torch, dist)
+            max(3, min(args.steps, 10)), 3, world, dev, torch, dist))
     # ---- CPU oracle baseline ----
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         n, t, cores = oracle_sample(wl, args.cpu_budget)

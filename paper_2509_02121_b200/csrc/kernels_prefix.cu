@@ -305,6 +305,9 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         const int trow = x * kSubRows + r;      // tile row
         const uint32_t lane_addr = tmem + ((uint32_t)(32 * wq) << 16);
         const bool valid_row = trow < T.nrows;
+        // causal prefill tile (tile_aux.z): this row (a prompt token) sees its request's first
+        // aux.w + trow/g + 1 suffix tokens; every other tile sees its whole token range
+        const int vis = aux.z > 0 ? aux.w + trow / a.g + 1 : 0x7fffffff;
         const int g = a.g;
         const int req = !valid_row ? 0 : aux.x >= 0 ? aux.x + trow / g : a.p.req_order[T.req_off + trow / g];
         const int head = T.kv_head * g + trow % g;
@@ -333,7 +336,8 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             if (threadIdx.x == 0) K1_TRACE(6, n);
             if (threadIdx.x == 128) K1_TRACE(14, n);
             ptx::tc_fence_after();
-            const int valid = min(kK1Tok, T.tok_end - (T.tok_begin + n * kK1Tok));
+            const int valid = min(min(kK1Tok, T.tok_end - (T.tok_begin + n * kK1Tok)),
+                                  vis - (T.tok_begin + n * kK1Tok));
             // the whole 128-column score row in registers: one TMEM round trip per n-tile
             uint32_t sr[kK1Tok];
             HALO_TMEM_LD32(s_addr, sr);

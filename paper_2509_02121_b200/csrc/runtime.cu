@@ -341,8 +341,18 @@ bool force_narrow() {
 // `virt` (prefill): the plan's rows are these virtual requests -- one per new prompt token,
 // with its request's leaf and the prefix of its suffix blocks up to and including the token
 // -- instead of the pool requests `reqs`.
+// Prefill groups: the rows [first, first + ntok) of `virt` are the new tokens of one request
+// whose suffix is `blocks` (len tokens); token t sees len - ntok + t + 1 suffix tokens.  When
+// the group has enough rows for the tensor cores, its causal part runs as K1 tiles over the
+// request's own blocks (and the rows' virtual suffixes are emptied for K2).
+struct CausalGroup {
+    int32_t first, ntok, len;
+    const std::vector<int32_t> *blocks;
+};
+
 halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
-                       const std::vector<Request> *virt = nullptr) {
+                       const std::vector<Request> *virt = nullptr,
+                       const std::vector<CausalGroup> *causal = nullptr) {
     halo_pool p = pl->pool;
     const auto &cfg = p->cfg;
     const int g = cfg.num_q_heads / cfg.num_kv_heads;
@@ -485,9 +495,24 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         }
         max_slots = std::max(max_slots, pl->req_nslots[i]);
     }
+    // causal K1 groups (prefill): one more partial slot for each of their rows
+    std::vector<char> causal_k1(causal ? causal->size() : 0, 0);
+    if (causal) {
+        for (size_t c = 0; c < causal->size(); ++c) {
+            const CausalGroup &cg = (*causal)[c];
+            if ((int64_t)cg.ntok * g < min_rows || cg.len > kK1MaxTileTok) continue;
+            causal_k1[c] = 1;
+            for (int32_t t = 0; t < cg.ntok; ++t) {
+                const int i = cg.first + t;
+                pl->req_nslots[i] += 1;
+                max_slots = std::max(max_slots, pl->req_nslots[i]);
+            }
+        }
+    }
     // 9./10. K1 node blocks and tiles
     pl->node_blocks.clear();
     pl->tiles.clear();
+    std::vector<int32_t> tile_causal;  // per tile: visible-token offset of its first row, or -1
     double k1_flops = 0, k1_bytes = 0;
     for (int i : pre_order) {
         PNode &n = ns[i];
@@ -512,11 +537,55 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
                     t.slot = n.slot_base + s;
                     t.node = i;
                     pl->tiles.push_back(t);
+                    tile_causal.push_back(-1);
                 }
     }
-    std::stable_sort(pl->tiles.begin(), pl->tiles.end(), [](const PrefixTile &a, const PrefixTile &b) {
-        return (a.tok_end - a.tok_begin) > (b.tok_end - b.tok_begin);
-    });
+    if (causal) {
+        // DFS position of every row (caller index -> position in req_order)
+        std::vector<int32_t> pos(nreq);
+        for (int r = 0; r < nreq; ++r) pos[pl->req_order[r]] = r;
+        for (size_t c = 0; c < causal->size(); ++c) {
+            if (!causal_k1[c]) continue;
+            const CausalGroup &cg = (*causal)[c];
+            const int32_t blk_off = (int32_t)pl->node_blocks.size();
+            pl->node_blocks.insert(pl->node_blocks.end(), cg.blocks->begin(), cg.blocks->end());
+            const int64_t rows = (int64_t)cg.ntok * g;
+            const int32_t base = cg.len - cg.ntok;  // suffix tokens before the prompt
+            for (int32_t t = 0; t < cg.ntok; ++t)
+                k1_flops += 4.0 * g * (base + t + 1) * D * hkv;
+            k1_bytes += (double)cg.len * hkv * D * 4 + (double)rows * hkv * D * 2 + (double)rows * hkv * (D + 1) * 4;
+            for (int64_t m0 = 0; m0 < rows; m0 += kK1Rows)
+                for (int j = 0; j < hkv; ++j) {
+                    PrefixTile t;
+                    t.req_off = pos[cg.first] + (int32_t)(m0 / g);
+                    t.nrows = (int32_t)std::min<int64_t>(kK1Rows, rows - m0);
+                    t.kv_head = j;
+                    t.tok_begin = 0;
+                    // the tile's last row sees base + (m0 + nrows)/g tokens: nothing after
+                    t.tok_end = std::min<int32_t>(cg.len, base + (int32_t)((m0 + t.nrows + g - 1) / g));
+                    t.blk_off = blk_off;
+                    t.slot = pl->req_nslots[cg.first] - 1;
+                    t.node = -1;
+                    pl->tiles.push_back(t);
+                    tile_causal.push_back(base + (int32_t)(m0 / g));
+                }
+        }
+    }
+    {
+        std::vector<size_t> idx(pl->tiles.size());
+        for (size_t k = 0; k < idx.size(); ++k) idx[k] = k;
+        std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+            return (pl->tiles[a].tok_end - pl->tiles[a].tok_begin) > (pl->tiles[b].tok_end - pl->tiles[b].tok_begin);
+        });
+        std::vector<PrefixTile> t2(idx.size());
+        std::vector<int32_t> c2(idx.size());
+        for (size_t k = 0; k < idx.size(); ++k) {
+            t2[k] = pl->tiles[idx[k]];
+            c2[k] = tile_causal[idx[k]];
+        }
+        pl->tiles.swap(t2);
+        tile_causal.swap(c2);
+    }
     // 10b. per-tile shortcuts that save K1 a dependent global load each: the caller index of
     // the tile's first request when its requests are consecutive caller indices (q rows are
     // then addressed directly), and the pool block of its first token when the node's blocks
@@ -532,7 +601,17 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         bool bc = true;
         for (int b = b0 + 1; b < b1 && bc; ++b) bc = pl->node_blocks[t.blk_off + b] == pl->node_blocks[t.blk_off + b - 1] + 1;
         if (bc) pl->tile_aux[4 * ti + 1] = pl->node_blocks[t.blk_off + b0];
+        if (tile_causal[ti] >= 0) {  // causal prefill tile: row r sees w + r/g + 1 tokens
+            pl->tile_aux[4 * ti + 2] = 1;
+            pl->tile_aux[4 * ti + 3] = tile_causal[ti];
+        }
     }
+    // rows whose causal part runs in K1 stream no suffix blocks in K2
+    std::vector<char> skip_suffix(nreq, 0);
+    if (causal)
+        for (size_t c = 0; c < causal->size(); ++c)
+            if (causal_k1[c])
+                for (int32_t t = 0; t < (*causal)[c].ntok; ++t) skip_suffix[(*causal)[c].first + t] = 1;
     // 11. K2 per-request block lists: folded path nodes root -> leaf, then the suffix
     pl->req_blk_off.assign(nreq + 1, 0);
     pl->req_blk.clear();
@@ -556,7 +635,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             ctx += n.node->ntok;
             if (!n.tensor) push_blocks(n.node->blocks, n.node->ntok);
         }
-        push_blocks(R[i]->blocks, R[i]->len);
+        if (!skip_suffix[i]) push_blocks(R[i]->blocks, R[i]->len);
         unshared += (double)ctx * hkv * D * 4;
     }
     pl->req_blk_off[nreq] = (int32_t)pl->req_blk.size();
@@ -570,89 +649,108 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         return pl->req_blk_off[a + 1] - pl->req_blk_off[a] > pl->req_blk_off[b + 1] - pl->req_blk_off[b];
     });
     // 12b. K2 schedule: static chunks, warp w takes chunks w, w + W, ...
+    // Work items: unit u = its n_u blocks followed by one merge item (the K3 epilogue), so
+    // units with few or no blocks (prefill rows whose causal part ran in K1) still spread
+    // over the warps.  Chunks are contiguous item ranges of about equal weight.
     {
         const int U = nreq * hkv;
-        int64_t W = (int64_t)p->num_sms * kK2WarpsWide;
+        const int64_t Ww = (int64_t)p->num_sms * kK2WarpsWide, Wn = (int64_t)p->num_sms * kK2WarpsNarrow;
         pl->k2_warps = kK2WarpsWide;
         pl->unit_boff.assign(U + 1, 0);
         for (int u = 0; u < U; ++u) {
             const int req = pl->unit_req[u / hkv];
             pl->unit_boff[u + 1] = pl->unit_boff[u] + (pl->req_blk_off[req + 1] - pl->req_blk_off[req]);
         }
-        const int64_t Btot = pl->unit_boff[U];
-        std::vector<int32_t> &lo = pl->chunk_lo;
-        lo.assign(1, 0);
-        // Cuts snapped to the nearest unit boundary, if the largest chunk stays within 5% of
-        // the equal share: whole units need no stream-K merge.
-        auto snap = [&](int64_t nw, std::vector<int32_t> &out) {
-            out.assign(1, 0);
-            size_t u = 0;
-            for (int64_t w = 1; w < nw; ++w) {
-                const int64_t b = w * Btot / nw;
-                while (u + 1 < pl->unit_boff.size() && pl->unit_boff[u + 1] <= b) ++u;
-                int64_t c = pl->unit_boff[u];
-                if (u + 1 < pl->unit_boff.size() && pl->unit_boff[u + 1] - b < b - c) c = pl->unit_boff[u + 1];
-                if (c > out.back() && c < Btot) out.push_back((int32_t)c);
+        const int64_t Btot = pl->unit_boff[U], Itot = Btot + U;
+        auto ui = [&](int64_t u) { return (int64_t)pl->unit_boff[u] + u; };  // items before unit u
+        auto nb = [&](int64_t u) { return (int64_t)pl->unit_boff[u + 1] - pl->unit_boff[u]; };
+        auto unit_of = [&](int64_t x) {  // unit owning item x < Itot
+            int64_t a = 0, b = U - 1;
+            while (a < b) {
+                const int64_t m = (a + b + 1) / 2;
+                if (ui(m) <= x) a = m; else b = m - 1;
             }
-            int64_t mx = Btot - out.back();
-            for (size_t i = 1; i < out.size(); ++i) mx = std::max<int64_t>(mx, out[i] - out[i - 1]);
-            return mx * 100 <= ceil_div(Btot, nw) * 105;
+            return a;
         };
-        std::vector<int32_t> cuts;
-        if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
-            for (int64_t x = pl->opt.k2_chunk_blocks; x < Btot; x += pl->opt.k2_chunk_blocks) lo.push_back((int32_t)x);
-        } else if (force_narrow() || (U < 2 * W && snap((int64_t)p->num_sms * kK2WarpsNarrow, cuts))) {
-            if (force_narrow()) {  // test hook: equal cuts over the narrow shape
-                cuts.assign(1, 0);
-                const int64_t Wn = (int64_t)p->num_sms * kK2WarpsNarrow;
-                for (int64_t w = 1; w < Wn; ++w) {
-                    const int64_t b = w * Btot / Wn;
-                    if (b > cuts.back() && b < Btot) cuts.push_back((int32_t)b);
-                }
+        // a cut never separates a unit's merge item from its last block (that chunk would
+        // visit the unit with no blocks)
+        auto push_cut = [&](std::vector<int64_t> &c, int64_t x) {
+            if (x > 0 && x < Itot) {
+                const int64_t u = unit_of(x);
+                if (nb(u) > 0 && x - ui(u) == nb(u)) ++x;
             }
+            if (x > c.back() && x < Itot) c.push_back(x);
+        };
+        auto equal_cuts = [&](int64_t nw) {
+            std::vector<int64_t> c(1, 0);
+            for (int64_t w = 1; w < nw; ++w) push_cut(c, w * Itot / nw);
+            c.push_back(Itot);
+            return c;
+        };
+        // cuts snapped to the nearest unit boundary; `balanced` if the largest chunk stays
+        // within 5% of the equal share (whole units: no stream-K merges)
+        auto snapped_cuts = [&](int64_t nw, bool &balanced) {
+            std::vector<int64_t> c(1, 0);
+            for (int64_t w = 1; w < nw && Itot > 0; ++w) {
+                const int64_t x = w * Itot / nw, u = unit_of(x);
+                const int64_t y = (x - ui(u) <= ui(u + 1) - x) ? ui(u) : ui(u + 1);
+                if (y > c.back() && y < Itot) c.push_back(y);
+            }
+            c.push_back(Itot);
+            int64_t mx = 0;
+            for (size_t k = 1; k < c.size(); ++k) mx = std::max<int64_t>(mx, c[k] - c[k - 1]);
+            balanced = mx * 100 <= ceil_div(Itot, nw) * 105;
+            return c;
+        };
+        std::vector<int64_t> cuts;
+        bool bal = false;
+        if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
+            cuts.assign(1, 0);
+            for (int64_t x = pl->opt.k2_chunk_blocks; x < Itot; x += pl->opt.k2_chunk_blocks) push_cut(cuts, x);
+            cuts.push_back(Itot);
+        } else if (force_narrow()) {  // test hook
+            pl->k2_warps = kK2WarpsNarrow;
+            cuts = equal_cuts(Wn);
+        } else if (U < 2 * Ww && (cuts = snapped_cuts(Wn, bal), bal)) {
             // few units per warp (stream-K pieces would dominate) and whole units divide
             // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
             pl->k2_warps = kK2WarpsNarrow;
-            W = (int64_t)p->num_sms * kK2WarpsNarrow;
-            lo = cuts;
-        } else if (snap(W, cuts)) {
-            lo = cuts;
         } else {
-            // static equal-bytes partition: warp w gets [w*Btot/W, (w+1)*Btot/W).  (A dynamic
-            // tail of small chunks was slower: per-chunk setup latencies.)
-            for (int64_t w = 1; w < W; ++w) {
-                const int64_t b = w * Btot / W;
-                if (b > lo.back() && b < Btot) lo.push_back((int32_t)b);
-            }
+            cuts = snapped_cuts(Ww, bal);
+            if (!bal) cuts = equal_cuts(Ww);  // equal item ranges (stream-K pieces)
         }
-        lo.push_back((int32_t)Btot);
-        if (lo.size() < 2) lo.push_back(0);
-        const int64_t nchunks = (int64_t)lo.size() - 1;
-        auto chunk_of = [&](int64_t xx) {  // chunk containing block index xx (Btot -> last)
-            if (xx >= Btot) return nchunks - 1;
-            return (int64_t)(std::upper_bound(lo.begin(), lo.end(), (int32_t)xx) - lo.begin()) - 1;
+        if (cuts.size() < 2) cuts = {0, Itot};
+        const int64_t nchunks = (int64_t)cuts.size() - 1;
+        auto block_at = [&](int64_t x) {  // global block index where item x starts
+            if (x >= Itot) return Btot;
+            const int64_t u = unit_of(x);
+            return (int64_t)pl->unit_boff[u] + std::min(x - ui(u), nb(u));
         };
-        pl->chunk_u0.assign(nchunks, U);
+        std::vector<int32_t> &lo = pl->chunk_lo;
+        lo.resize(nchunks + 1);
+        for (int64_t c = 0; c <= nchunks; ++c) lo[c] = (int32_t)block_at(cuts[c]);
+        auto chunk_of = [&](int64_t x) {  // chunk containing item x
+            return (int64_t)(std::upper_bound(cuts.begin(), cuts.end(), x) - cuts.begin()) - 1;
+        };
+        pl->chunk_u0.assign(nchunks, 0);
         pl->chunk_u1.assign(nchunks, 0);
+        for (int64_t c = 0; c < nchunks && U > 0; ++c) {
+            if (cuts[c + 1] <= cuts[c]) continue;
+            pl->chunk_u0[c] = (int32_t)unit_of(cuts[c]);
+            pl->chunk_u1[c] = (int32_t)unit_of(cuts[c + 1] - 1) + 1;
+        }
         pl->unit_nseg.resize(U);
         pl->unit_seg.resize(U);
         pl->unit_chunk0.resize(U);
         int32_t nseg_total = 0;
         for (int uu = 0; uu < U; ++uu) {
-            const int64_t b = pl->unit_boff[uu], e = pl->unit_boff[uu + 1];
-            const int64_t c0 = chunk_of(b), c1 = e > b ? chunk_of(e - 1) : c0;
-            for (int64_t cc = c0; cc <= c1; ++cc) {
-                pl->chunk_u0[cc] = std::min(pl->chunk_u0[cc], uu);
-                pl->chunk_u1[cc] = std::max(pl->chunk_u1[cc], uu + 1);
-            }
+            const int64_t c0 = chunk_of(ui(uu)), c1 = chunk_of(ui(uu + 1) - 1);
             const int nseg = (int)(c1 - c0 + 1);
             pl->unit_chunk0[uu] = (int32_t)c0;
             pl->unit_nseg[uu] = nseg;
             pl->unit_seg[uu] = nseg > 1 ? nseg_total : -1;
             if (nseg > 1) nseg_total += nseg;
         }
-        for (int64_t cc = 0; cc < nchunks; ++cc)
-            if (pl->chunk_u0[cc] >= pl->chunk_u1[cc]) pl->chunk_u0[cc] = pl->chunk_u1[cc] = 0;
         pl->nseg_total = nseg_total;
         pl->chunk_info.resize((size_t)nchunks * 4);
         for (int64_t cc = 0; cc < nchunks; ++cc) {
@@ -1432,8 +1530,10 @@ halo_status halo_prefill_plan(halo_pool p, int32_t nreq, const int64_t *reqs, co
         if (total > INT32_MAX / 64) return fail(HALO_EINVAL, "too many prefill tokens");
     }
     virt.reserve(total);
+    std::vector<CausalGroup> groups;
     for (int i = 0; i < nreq; ++i) {
         const Request &r = p->requests[reqs[i]];
+        groups.push_back({(int32_t)virt.size(), ntok[i], r.len, &r.blocks});
         for (int32_t t = 0; t < ntok[i]; ++t) {
             Request v;
             v.leaf = r.leaf;
@@ -1447,7 +1547,7 @@ halo_status halo_prefill_plan(halo_pool p, int32_t nreq, const int64_t *reqs, co
     halo_plan pl = fresh ? new halo_plan_s() : *inout;
     pl->pool = p;
     pl->opt = opt ? *opt : halo_plan_options{};
-    halo_status st = build_plan(pl, (int32_t)total, nullptr, &virt);
+    halo_status st = build_plan(pl, (int32_t)total, nullptr, &virt, &groups);
     if (st == HALO_OK) st = upload_plan(pl, (cudaStream_t)stream);
     if (st != HALO_OK) {
         if (fresh) {

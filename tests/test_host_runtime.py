@@ -246,24 +246,58 @@ def test_k2_chunk_schedule_covers_every_block_once(cfg, kw, cb):
 
 def test_prefill_plan_rows_are_causal_virtual_requests():
     """halo_prefill_plan (NEXT-4): one row per new prompt token; token t of request i sees
-    the first len - ntok + t + 1 suffix tokens (its K2 block list grows with t)."""
+    the first len - ntok + t + 1 suffix tokens.  With few rows the causal part streams in K2
+    (the row's block list grows with t); with enough rows (ntok x g >= min_rows) it becomes
+    causal K1 tiles over the request's own blocks and K2 only merges."""
     p = host_pool(layers=1, hkv=2, hq=8, cap=400)
     a = p.register_prefix(-1, 100)
     r1, r2 = p.open_request(a), p.open_request(-1)
     p.append([r1, r2], [20, 40])
+    # all in K2 (min_rows huge): the prefix is folded (+7 blocks on r1's rows)
+    pl = p.prefill_plan([r1, r2], [20, 33], PlanOptions(100000, 0, 0, 0))
+    info = pl.info()
+    assert info["nreq"] == 53 and info["k1_tiles"] == 0
+    nblk = np.diff(pl.export("req_blk_off"))
+    want = [(n + 15) // 16 + 7 for n in range(1, 21)] + [(n + 15) // 16 for n in range(8, 41)]
+    assert list(nblk) == want
+    pl.destroy()
+    # default: 20 x 4 = 80 and 33 x 4 = 132 rows >= 64 -> causal K1 tiles, nothing for K2
     pl = p.prefill_plan([r1, r2], [20, 33])
     info = pl.info()
-    assert info["nreq"] == 53
-    off = pl.export("req_blk_off")
-    nblk = np.diff(off)
-    # r1 rows: suffix lengths 1..20; r2 rows: 8..40 (no prefix: the whole context is K2's)
-    want = [(n + 15) // 16 for n in range(1, 21)] + [(n + 15) // 16 for n in range(8, 41)]
-    if info["tensor_nodes"] == 0:       # prefix folded into K2: +7 blocks for r1's rows
-        want = [w + 7 for w in want[:20]] + want[20:]
-    assert list(nblk) == want
+    assert list(np.diff(pl.export("req_blk_off"))) == [0] * 53
+    tiles = pl.export("tiles").reshape(-1, 8)
+    causal = [t for t in tiles if t[7] == -1]
+    assert len(causal) == 2 * 2                      # (r1, r2) x 2 kv heads, one m-tile each
+    assert sorted(int(t[1]) for t in causal) == [80, 80, 132, 132]
+    assert sorted(int(t[4]) for t in causal) == [20, 20, 40, 40]   # token range = visible max
+    nsl = pl.export("req_nslots")
+    assert list(nsl[:20]) == [2] * 20 and list(nsl[20:]) == [1] * 33   # prefix + causal slots
     pl.destroy()
     for bad in ([0, 1], [21, 1], [1, 41]):
         with pytest.raises(halo.HaloError) as e:
             p.prefill_plan([r1, r2], bad)
         assert e.value.name == "HALO_EINVAL"
+    p.destroy()
+
+
+def test_k2_schedule_spreads_blockless_units_over_warps():
+    """Prefill rows whose causal part runs in K1 leave K2 with merge-only units: the item
+    schedule (blocks + one merge item per unit) must still spread them over many chunks,
+    each unit in exactly one chunk, chunk unit ranges tiling [0, U)."""
+    p = host_pool(layers=1, hkv=2, hq=8, cap=4000)
+    a = p.register_prefix(-1, 256)
+    reqs = [p.open_request(a) for _ in range(64)]
+    p.append(reqs, [40] * 64)
+    pl = p.prefill_plan(reqs, [40] * 64)
+    boff = pl.export("unit_boff")
+    assert boff[-1] == 0                        # no blocks left for K2
+    u0, u1, nseg, clo = pl.export("chunk_u0"), pl.export("chunk_u1"), pl.export("unit_nseg"), pl.export("chunk_lo")
+    U = len(boff) - 1
+    assert U == 64 * 40 * 2 and len(u0) >= 1000  # ~one merge per chunk at 148 x 12 warps
+    assert all(n == 1 for n in nseg)
+    cover = np.zeros(U, dtype=np.int32)
+    for c in range(len(u0)):
+        cover[u0[c]:u1[c]] += 1
+    assert np.all(cover == 1) and np.all(clo == 0)
+    pl.destroy()
     p.destroy()

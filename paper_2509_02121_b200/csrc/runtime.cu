@@ -1579,6 +1579,9 @@ halo_status halo_decode_run(halo_plan pl, int32_t layer, const void *q, float *o
     if (!q || !out) return fail(HALO_EINVAL, "null q/out");
     if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)p->cfg.head_dim);
     DeviceGuard dg(p);
+    // the stream now reads pool blocks: later frees wait for it (host bookkeeping only, so
+    // this is safe under stream capture)
+    note_stream(p, (cudaStream_t)stream);
     return run_layer(pl, layer, q, out, lse, scale, (cudaStream_t)stream);
     HALO_GUARD_END
 }
@@ -1594,6 +1597,7 @@ halo_status halo_decode_run_stages(halo_plan pl, int32_t layer, int32_t mask, co
     if (!q || ((mask & 2) && !out)) return fail(HALO_EINVAL, "null q/out");
     if (!(scale > 0.f)) scale = 1.0f / sqrtf((float)p->cfg.head_dim);
     DeviceGuard dg(p);
+    note_stream(p, (cudaStream_t)stream);
     return run_layer(pl, layer, q, out, lse, scale, (cudaStream_t)stream, mask);
     HALO_GUARD_END
 }
@@ -1640,6 +1644,7 @@ halo_status halo_decode_layers(halo_plan pl, int32_t nlayers, const void *q, flo
         if ((st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * nlayers * 4)) != HALO_OK) return st;
         dlse = pl->l_stage;
     }
+    note_stream(p, s);
     for (int l = 0; l < nlayers; ++l) {
         st = run_layer(pl, l, static_cast<const uint16_t *>(dq) + q_layer * l, dout + o_layer * l,
                        dlse ? dlse + rows * l : nullptr, scale, s);

@@ -456,3 +456,47 @@ def test_k2_narrow_launch_shape_on_every_head_layout():
     env = dict(os.environ, HALO_K2_FORCE_NARROW="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "narrow ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_maximum_sizes_long_prefix_and_long_suffix():
+    """Edge sizes: a 32k-token prefix node (the largest node of BASELINE configs[4]; split
+    into many K1 tiles), a 16k-token private suffix (the longest context of PAPER.md:685,
+    one K2 unit cut into many stream-K pieces), requests without a prefix, and a 1-token
+    suffix; sampled rows vs the oracle."""
+    from synth.workloads import NodeSpec, RequestSpec, Workload
+    nodes = [NodeSpec(0, -1, 32768), NodeSpec(1, -1, 1000)]
+    reqs = [RequestSpec(i, 0, 7) for i in range(70)] + [RequestSpec(70, 1, 16383),
+                                                       RequestSpec(71, -1, 16383),
+                                                       RequestSpec(72, -1, 0),
+                                                       RequestSpec(73, 0, 0)]
+    wl = Workload("maxsize", 1, 32, 8, 128, nodes, reqs, 9)
+    check(wl, sample=[0, 33, 69, 70, 71, 72, 73])
+
+
+def test_decode_run_is_cuda_graph_capturable():
+    """halo_decode_run is documented graph-capturable: capture two layers (K1 + K2 with
+    programmatic dependent launches) in a CUDA graph, replay, compare with eager runs."""
+    wl = make_config("fanout", layers=2, nreq=64, prefix=600, suffix=30)
+    ld = load(wl, DEV)
+    append_step(ld, wl, 0, DEV)
+    plan = ld.pool.plan(ld.req_ids)
+    q = wl.q(0, "cuda")
+    eager = torch.empty((2, wl.nreq, wl.hq, wl.d), device="cuda")
+    for l in range(2):
+        plan.run(l, q[l], eager[l])
+    torch.cuda.synchronize()
+    out = torch.zeros_like(eager)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for l in range(2):
+                plan.run(l, q[l], out[l], stream=s)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, eager)
+    del g
+    cleanup(ld, plan)

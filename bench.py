@@ -411,6 +411,9 @@ def main():
     # ---- host paging of the template node (NEXT-2) ----
     if not args.no_migration and not args.profile:
         guarded("paging", lambda: measure_paging(pool, ld, wl, torch))
+    # ---- cost-model relocation planner (NEXT-1), host-side ----
+    if not args.profile:
+        guarded("relocation", lambda: measure_relocation(halo, extra.get("migration", {})))
     # ---- continuous batching under churn (NEXT-3) ----
     if not args.no_e2e and not args.profile:
         guarded("continuous", lambda: measure_continuous(halo, wl, dev, torch, min(args.steps, 30)))
@@ -608,6 +611,38 @@ def measure_paging(pool, ld, wl, torch):
                                         "peak_source": "pinned cudaMemcpy H2D of the same bytes, this run"}},
             "recompute_estimate_ms": prefill_ms,
             "transfer_vs_recompute": prefill_ms / t_fetch}
+
+
+def measure_relocation(halo, mig):
+    """halo_place_groups (Alg. 1 + §3.2 costs) on the C3 batch: 64 templates x
+    8192-token contexts (256 requests each, 32 layers) whose KV was all prefilled on worker
+    0, placed over 8 workers for a 256-step decode horizon.  e_v from the K1/K2 rooflines at
+    the measured peaks; p_v = template KV bytes / link rate (the NCCL GB/s measured above
+    when N > 1, else the nominal per-direction NVLink rate).  Host time of the native
+    planner, and the moves it emits (executed by halo_migrate_send/recv on a multi-GPU box)."""
+    import time
+    from paper_2509_02121_b200.relocation import plan_relocation
+    from synth import make_config
+    hbm, tc = peaks()[:2]
+    link = mig.get("GB/s", 0.0) * 1e9 if "nvlink_roofline" in mig else 900e9
+    wl = make_config("analytics", templates=64)
+    out = {}
+    for w in (1, 8, 64):
+        t0 = time.perf_counter()
+        groups, items, res = plan_relocation(wl, [0] * 64, workers=8, link_bytes_per_s=link,
+                                             beam_width=w, steps=256, tc_flops=tc * 1e12,
+                                             hbm_bps=hbm * 1e9, max_replicas=8)
+        dt = time.perf_counter() - t0
+        moved = sum(items[m[0]]["kv_bytes"] for m in res["moves"])
+        out[f"beam{w}"] = {"planner_ms": dt * 1e3, "makespan_s": res["cost"],
+                           "moves": len(res["moves"]), "bytes_moved": moved,
+                           "per_worker_groups": [sum(d in ws for ws in res["workers"]) for d in range(8)]}
+    total = sum(it["exec_s"] for it in items)
+    out.update({"what": "C3 batch (64 templates, all KV on worker 0) placed over 8 workers, "
+                        "256 decode steps; planner = native beam search (host)",
+                "link_GBps": link / 1e9, "all_on_one_worker_s": total,
+                "lower_bound_s": total / 8})
+    return out
 
 
 def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):

@@ -286,6 +286,67 @@ halo_status halo_node_residency(halo_pool pool, int64_t node, int32_t *on_device
  * evictions made so far stay). */
 halo_status halo_pool_evict_lru(halo_pool pool, int64_t want_free, void *stream, int32_t *n_evicted);
 
+/* ------------------------------------------------------------------ relocation planner
+ * Cost-model placement of prefix groups on workers (GPUs): PAPER.md Alg. 1 (§3.2, "Beam
+ * Search with Incremental Cost") with the cost functions of §3.2 "Cost Functions"
+ * (PAPER.md:315-332).  An item is one prefix group: a prefix tree (its nodes' KV) with the
+ * decode requests under it -- the operator whose placement decides where its KV lives.
+ * Host-only (no device work); the caller executes the returned moves with
+ * halo_migrate_send/recv (another GPU), halo_prefix_clone (same GPU) or halo_prefix_fetch
+ * (host arena).  Readings (DESIGN.md §5 "Relocation planner"):
+ *   - e_v = exec_s, the item's decode-attention time on one worker;
+ *   - p_v = context preparation on worker d: 0 if d == home, kv_bytes / link_bytes_per_s if
+ *     another worker holds the KV (relocation over NVLink), prep_s if none does (host
+ *     fetch or prefill);  gamma_v = sigma_v = lambda_v = 1 (e_v already counts prefix
+ *     sharing; no model weights or retrieval state move on this path);
+ *   - C_a^d = sum_{v on d} e_v / k_v^beta + p_v(d);  C_a = max_d C_a^d;
+ *     C_r = (sum of e_v over unassigned items) / m^beta;  Cost = C_a + C_r;
+ *   - V_r = the ops_per_iter unassigned items of largest e_v (ties: lower index) -- the
+ *     paper's "top-|D| ready operators"; items are independent (no DAG edges between
+ *     prefix groups), so every unassigned item is ready;
+ *   - replication over k > 1 workers (queries partitioned over replicas) is offered only
+ *     when fewer items remain unassigned than there are workers and e_v >= (sum of all
+ *     e_v) / workers (the paper's conditions (i), (ii)); the replica set is the home worker
+ *     (if any) plus the least-loaded other workers of the partial assignment;
+ *   - ties between equal-cost candidates: the lexicographically smaller assignment. */
+typedef struct {
+    double exec_s;         /* e_v >= 0: decode-attention seconds on one worker          */
+    double kv_bytes;       /* bytes one relocation of the item's KV moves (>= 0)        */
+    double prep_s;         /* p_v when no worker holds the KV (home == -1), >= 0        */
+    int32_t home;          /* worker holding the KV now, or -1                          */
+    int32_t max_replicas;  /* >= 1; 1 = single-assigned                                 */
+} halo_place_item;
+
+typedef struct {
+    int32_t workers;          /* m = |D|, 1..64                                          */
+    int32_t beam_width;       /* w >= 1                                                  */
+    int32_t ops_per_iter;     /* |V_r| cap per iteration, 1..workers                     */
+    int32_t reserved;
+    double beta;              /* parallelism decay, >= 0                                 */
+    double link_bytes_per_s;  /* measured relocation rate, > 0                           */
+} halo_place_config;
+
+typedef struct {
+    int32_t item;             /* index into items                                        */
+    int32_t src;              /* worker sending the KV; -1 = prepare from host / prefill */
+    int32_t dst;              /* worker receiving it                                     */
+    int32_t mode;             /* 0 = MOVE (src releases after), 1 = COPY                 */
+    double seconds;           /* the p_v this move was costed at                         */
+} halo_place_move;
+
+/* Run the beam search.  items: HOST array of n >= 1.  Outputs (HOST):
+ *   worker_mask[n]  bit d set <=> item placed on worker d (popcount = its replicas);
+ *   load[workers]   (nullable) final C_a^d;   *cost: final Cost (= C_a, nothing unassigned);
+ *   moves (nullable, room for move_cap) and *n_moves: the relocations that realise the
+ *   placement -- for an item with home h >= 0, one transfer h -> d per placed worker d != h,
+ *   COPY except the last when h is not in the placement (MOVE); for home -1, one prepare
+ *   (src -1, COPY) per placed worker.  Moves are ordered by item, then worker.
+ * EINVAL on a bad argument or when one iteration would enumerate more than 2^20
+ * candidates; ENOMEM if move_cap is too small (*n_moves still receives the count). */
+halo_status halo_place_groups(const halo_place_config *cfg, int32_t n, const halo_place_item *items,
+                              uint64_t *worker_mask, double *load, double *cost,
+                              halo_place_move *moves, int32_t move_cap, int32_t *n_moves);
+
 #ifdef __cplusplus
 }
 #endif

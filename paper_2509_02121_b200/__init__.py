@@ -7,7 +7,7 @@ library's CUDA kernels; there is no CPU fallback -- importing this package witho
 built library raises.  torch is used only for device memory and streams.
 """
 from .abi import (HaloError, Pool, Plan, PlanOptions, lib_path, load_library, comm_unique_id,
-                  STATUS)
+                  place_groups, STATUS)
 
 __all__ = ["HaloError", "Pool", "Plan", "PlanOptions", "lib_path", "load_library",
-           "comm_unique_id", "STATUS"]
+           "comm_unique_id", "place_groups", "STATUS"]

@@ -40,6 +40,20 @@ class PlanInfo(C.Structure):
                 ("unshared_bytes", C.c_double)]
 
 
+class PlaceItem(C.Structure):
+    _fields_ = [("exec_s", C.c_double), ("kv_bytes", C.c_double), ("prep_s", C.c_double),
+                ("home", _i32), ("max_replicas", _i32)]
+
+
+class PlaceConfig(C.Structure):
+    _fields_ = [("workers", _i32), ("beam_width", _i32), ("ops_per_iter", _i32), ("reserved", _i32),
+                ("beta", C.c_double), ("link_bytes_per_s", C.c_double)]
+
+
+class PlaceMove(C.Structure):
+    _fields_ = [("item", _i32), ("src", _i32), ("dst", _i32), ("mode", _i32), ("seconds", C.c_double)]
+
+
 SIGNATURES = {
     "halo_last_error": (C.c_char_p, []),
     "halo_abi_version": (_i32, []),
@@ -77,6 +91,9 @@ SIGNATURES = {
     "halo_prefix_fetch": (_i32, [_p, _i64, _p]),
     "halo_node_residency": (_i32, [_p, _i64, C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]),
     "halo_pool_evict_lru": (_i32, [_p, _i64, _p, C.POINTER(C.c_int32)]),
+    "halo_place_groups": (_i32, [C.POINTER(PlaceConfig), _i32, C.POINTER(PlaceItem),
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(PlaceMove), _i32, C.POINTER(C.c_int32)]),
 }
 
 _lib = None
@@ -155,6 +172,37 @@ def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _call("halo_comm_unique_id", buf)
     return buf.raw
+
+
+def place_groups(items, workers: int, beam_width: int = 16, ops_per_iter: int = 1,
+                 beta: float = 1.0, link_bytes_per_s: float = 1e11) -> dict:
+    """halo_place_groups: the relocation planner (Alg. 1 with the §3.2 costs).
+    items: sequence of dicts with exec_s, kv_bytes, prep_s (default 0), home (default -1),
+    max_replicas (default 1).  Returns {"workers": [list of worker indices per item],
+    "masks", "load", "cost", "moves": [(item, src, dst, mode, seconds)]}."""
+    n = len(items)
+    arr = (PlaceItem * max(n, 1))()
+    for i, it in enumerate(items):
+        arr[i] = PlaceItem(float(it["exec_s"]), float(it.get("kv_bytes", 0.0)),
+                           float(it.get("prep_s", 0.0)), int(it.get("home", -1)),
+                           int(it.get("max_replicas", 1)))
+    cfg = PlaceConfig(int(workers), int(beam_width), int(ops_per_iter), 0, float(beta),
+                      float(link_bytes_per_s))
+    masks = (C.c_uint64 * max(n, 1))()
+    load = (C.c_double * max(int(workers), 1))()
+    cost = C.c_double(0.0)
+    cap = max(n * max(int(workers), 1), 1)
+    moves = (PlaceMove * cap)()
+    nm = C.c_int32(0)
+    _call("halo_place_groups", C.byref(cfg), n, arr, masks, load, C.byref(cost), moves, cap,
+          C.byref(nm))
+    ms = [int(masks[i]) for i in range(n)]
+    return {"masks": ms,
+            "workers": [[d for d in range(workers) if m >> d & 1] for m in ms],
+            "load": [load[d] for d in range(workers)],
+            "cost": cost.value,
+            "moves": [(moves[i].item, moves[i].src, moves[i].dst, moves[i].mode, moves[i].seconds)
+                      for i in range(nm.value)]}
 
 
 class Pool:

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libhalo_attn.so")
-SOURCES = ["runtime.cu", "kernels_prefix.cu", "kernels_suffix.cu", "kernels_copy.cu"]
+SOURCES = ["runtime.cu", "kernels_prefix.cu", "kernels_suffix.cu", "kernels_copy.cu", "placement.cpp"]
 HEADERS = ["halo_internal.h", "ptx.h", "runtime.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,7 +36,7 @@ def build(verbose: bool = False, force: bool = False, extra: list[str] | None = 
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD_, src.replace(".cu", ".o"))
+        o = os.path.join(BUILD_, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-c", s, "-o", o]

@@ -27,6 +27,17 @@ halo_status fail(halo_status st, const char *fmt, ...) {
     return st;
 }
 
+}  // namespace
+
+namespace halo {
+halo_status report_error(halo_status st, const char *msg) {
+    g_err = msg;
+    return st;
+}
+}  // namespace halo
+
+namespace {
+
 #define HALO_CUDA(expr)                                                                       \
     do {                                                                                      \
         cudaError_t e_ = (expr);                                                              \

@@ -92,6 +92,9 @@ inline void PinRing::release() {
     }
 }
 
+// Set the calling thread's halo_last_error() text (for ABI entry points outside runtime.cu).
+halo_status report_error(halo_status st, const char *msg);
+
 }  // namespace halo
 
 struct halo_pool_s {

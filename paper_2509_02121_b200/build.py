@@ -66,7 +66,7 @@ def build(verbose: bool = False, force: bool = False, extra: list[str] | None = 
 
 def build_trace() -> str:
     """Debug variant with the K1 timeline trace (never used by tests or bench)."""
-    return build(extra=["-DHALO_K1_TRACE"], lib=os.path.join(PKG, "libhalo_attn_trace.so"),
+    return build(extra=["-DHALO_K1_TRACE", "-DHALO_K2_TRACE"], lib=os.path.join(PKG, "libhalo_attn_trace.so"),
                  build_dir=os.path.join(PKG, "_build_trace"))
 
 

@@ -34,6 +34,25 @@
 #include "halo_internal.h"
 #include "ptx.h"
 
+#ifdef HALO_K2_TRACE
+// Debug timeline: g_k2_trace[gw * 4 + e] = %globaltimer (ns) of global warp gw at event e:
+// 0 entry, 1 first K/V stage landed, 2 K1 complete (griddepcontrol.wait returned), 3 exit.
+__device__ unsigned long long *g_k2_trace = nullptr;
+#define K2_TRACE(gw, ev)                                                                \
+    do {                                                                                \
+        if (g_k2_trace && lane == 0) {                                                  \
+            unsigned long long t_;                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+            g_k2_trace[(gw) * 4 + (ev)] = t_;                                           \
+        }                                                                               \
+    } while (0)
+extern "C" int halo_debug_k2_trace(void *buf) {
+    return (int)cudaMemcpyToSymbol(g_k2_trace, &buf, sizeof(buf));
+}
+#else
+#define K2_TRACE(gw, ev) do { } while (0)
+#endif
+
 namespace halo {
 namespace {
 
@@ -217,6 +236,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     const bool head_writer = (c % (LPT / G)) == 0;
     const int gw = blockIdx.x * kWarps + warp;
     if (gw >= P.nwarps) return;
+    K2_TRACE(gw, 0);
     const uint16_t *pk = a.pool_k + a.layer_off;
     const uint16_t *pv = a.pool_v + a.layer_off;
 
@@ -291,6 +311,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     auto wait_k1 = [&]() {
         if (!k1_ready) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
+            K2_TRACE(gw, 2);
             k1_ready = true;
         }
     };
@@ -353,6 +374,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                     fill();
                     const int st = c_count % ST;
                     ptx::mbar_wait(&full[st], (c_count / ST) & 1);
+#ifdef HALO_K2_TRACE
+                    if (c_count == 0) K2_TRACE(gw, 1);
+#endif
                     const int ntok = snt[st];
                     const uint8_t *kb = ws + st * S::STAGE;
                     const uint8_t *vb = kb + S::SLAB;
@@ -545,6 +569,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             __syncwarp();
         }
     }
+    K2_TRACE(gw, 3);
 }
 
 template <int D, int G, int kWarps, int kStages>

@@ -251,7 +251,7 @@ def test_planner_moves_execute_and_decode_bit_identically():
     p0 = ld.pool
     p1 = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, blocks_needed(wl), 0)
     groups, items, res = plan_relocation(wl, [0] * 4, workers=2, link_bytes_per_s=1e12,
-                                         beam_width=16)
+                                         beam_width=16, steps=10000)
     assert sorted(len(w) for w in res["workers"]) == [1, 1, 1, 1]
     assert sum(w == [1] for w in res["workers"]) == 2
     q = wl.q(0, "cuda")
@@ -265,13 +265,18 @@ def test_planner_moves_execute_and_decode_bit_identically():
         pl.destroy()
         return out
 
+    sk, sv = wl.suffix_kv("cuda")              # [L][sum S][Hkv][d]
+    nk, nv = wl.new_kv(0, "cuda")              # [L][R][Hkv][d]
+    off = wl.suffix_offsets
+
     def open_group(pool, nmap, rows):
         reqs = [pool.open_request(nmap[wl.requests[r].leaf]) for r in rows]
-        for rid, r in zip(reqs, rows):
-            k, v = wl.suffix_kv("cuda", request=r)
-            pool.append([rid], [wl.requests[r].suffix], k, v)
-            kn, vn = wl.new_kv(0, "cuda", request=r)
-            pool.append([rid], [1], kn, vn)
+        tok = torch.tensor([t for r in rows for t in range(int(off[r]), int(off[r + 1]))], device="cuda")
+        pool.append(reqs, [wl.requests[r].suffix for r in rows], sk.index_select(1, tok).contiguous(),
+                    sv.index_select(1, tok).contiguous())
+        idx = torch.tensor(rows, device="cuda")
+        pool.append(reqs, [1] * len(rows), nk.index_select(1, idx).contiguous(),
+                    nv.index_select(1, idx).contiguous())
         return reqs
 
     for rid in ld.req_ids:

@@ -1,4 +1,11 @@
-"""Per-warp timeline of K2 (debug build): start, first block arrived, end (us)."""
+"""Per-warp timeline of K2 (debug build with -DHALO_K2_TRACE): entry, first K/V stage
+landed, K1 complete (griddepcontrol.wait returned), exit -- in us from the earliest entry.
+
+Two runs on the chosen config (CFG=fanout|tree|analytics, LAYERS):
+  alone : K2 by itself after an L2 flush (K1's partials already written)
+  pdl   : K1 then K2 back to back (programmatic dependent launch), as the headline runs
+Usage (GPU box): python tools/k2_trace.py
+"""
 import ctypes
 import os
 import sys
@@ -17,39 +24,57 @@ from paper_2509_02121_b200.loader import append_step, load  # noqa: E402
 from synth import make_config  # noqa: E402
 
 
+def stats(name, v):
+    v = v[np.isfinite(v)]
+    if v.size == 0:
+        return f"{name:12s} (none)"
+    return (f"{name:12s} min={v.min():7.2f} p10={np.percentile(v, 10):7.2f} p50={np.median(v):7.2f} "
+            f"p90={np.percentile(v, 90):7.2f} max={v.max():7.2f}")
+
+
 def main():
-    wl = make_config(os.environ.get("CFG", "fanout"), layers=int(os.environ.get("LAYERS", "2")))
+    cfg = os.environ.get("CFG", "fanout")
+    wl = make_config(cfg, layers=int(os.environ.get("LAYERS", "2")))
     ld = load(wl, 0)
     append_step(ld, wl, 0, 0)
     plan = ld.pool.plan(ld.req_ids)
+    info = plan.info()
     q = wl.q(0, "cuda:0")
     out = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda:0")
     lib = halo.load_library()
     lib.halo_debug_k2_trace.argtypes = [ctypes.c_void_p]
-    W = 148 * 12
+    W = 148 * 16
     buf = torch.zeros(W * 4, dtype=torch.int64, device="cuda:0")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda:0")
-    for it in range(4):
-        plan.run_stages(1, 1, q[1], out)
-        flush.zero_()
-        buf.zero_()
-        lib.halo_debug_k2_trace(ctypes.c_void_p(buf.data_ptr()))
-        plan.run_stages(1, 2, q[1], out)
-        lib.halo_debug_k2_trace(ctypes.c_void_p(0))
-        torch.cuda.synchronize()
-    t = buf.view(W, 4).cpu().numpy().astype(np.float64)
-    t0 = t[:, 0].min()
-    t = (t - t0) / 1e3
-    print(f"warps={W} kernel span={t[:, 2].max():.2f} us")
-    for name, col in [("start", 0), ("first data", 1), ("end", 2)]:
-        v = t[:, col]
-        print(f"{name:11s} min={v.min():7.2f} p10={np.percentile(v,10):7.2f} p50={np.median(v):7.2f} "
-              f"p90={np.percentile(v,90):7.2f} max={v.max():7.2f}")
-    ends = t[:, 2].reshape(-1, 12).max(axis=1)
-    print("per-CTA end: min %.2f median %.2f max %.2f" % (ends.min(), np.median(ends), ends.max()))
-    order = np.argsort(ends)
-    print("slowest CTAs", order[-8:], ends[order[-8:]])
-    print("fastest CTAs", order[:8], ends[order[:8]])
+    print(f"{cfg}: k1_tiles={info['k1_tiles']} k2_units={info['k2_units']} k2_bytes={info['k2_bytes']:.3e}")
+    for mode in ("alone", "pdl"):
+        for it in range(4):
+            if mode == "alone":
+                plan.run_stages(1, 1, q[1], out)
+            flush.zero_()
+            buf.zero_()
+            lib.halo_debug_k2_trace(ctypes.c_void_p(buf.data_ptr()))
+            plan.run_stages(1, 2 if mode == "alone" else 3, q[1], out)
+            lib.halo_debug_k2_trace(ctypes.c_void_p(0))
+            torch.cuda.synchronize()
+        t = buf.view(W, 4).cpu().numpy().astype(np.float64)
+        used = t[:, 0] > 0
+        t = t[used]
+        t[t == 0] = np.nan
+        t0 = np.nanmin(t[:, 0])
+        t = (t - t0) / 1e3
+        span = np.nanmax(t[:, 3])
+        print(f"-- {mode}: warps={used.sum()} span={span:.2f} us  "
+              f"(k2 bytes / span = {info['k2_bytes'] / span / 1e3:.0f} GB/s)")
+        for name, col in [("entry", 0), ("first data", 1), ("k1 done", 2), ("exit", 3)]:
+            print(stats(name, t[:, col]))
+        print(stats("busy", t[:, 3] - t[:, 0]))
+        ncta_warps = int(os.environ.get("K2_WARPS", "0")) or None
+        if ncta_warps:
+            ends = t[:, 3][: (len(t) // ncta_warps) * ncta_warps].reshape(-1, ncta_warps).max(axis=1)
+            print("per-CTA exit: min %.2f median %.2f max %.2f" % (ends.min(), np.median(ends), ends.max()))
+    plan.destroy()
+    ld.pool.destroy()
 
 
 if __name__ == "__main__":

@@ -340,6 +340,15 @@ int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_
     return best_c;
 }
 
+// Experiment hook (HALO_K2_SMS=n): K2's schedule and grid use n SMs instead of all.
+int k2_sms(halo_pool p) {
+    static const int n = [] {
+        const char *e = getenv("HALO_K2_SMS");
+        return e ? atoi(e) : 0;
+    }();
+    return (n > 0 && n < p->num_sms) ? n : p->num_sms;
+}
+
 // Test hook (HALO_K2_FORCE_NARROW=1): always use K2's narrow launch shape.
 bool force_narrow() {
     static const bool f = [] {
@@ -665,7 +674,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     // over the warps.  Chunks are contiguous item ranges of about equal weight.
     {
         const int U = nreq * hkv;
-        const int64_t Ww = (int64_t)p->num_sms * kK2WarpsWide, Wn = (int64_t)p->num_sms * kK2WarpsNarrow;
+        const int64_t Ww = (int64_t)k2_sms(p) * kK2WarpsWide, Wn = (int64_t)k2_sms(p) * kK2WarpsNarrow;
         pl->k2_warps = kK2WarpsWide;
         pl->unit_boff.assign(U + 1, 0);
         for (int u = 0; u < U; ++u) {
@@ -937,7 +946,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
     dv.seg_o = pl->segbuf;
     dv.seg_ml = pl->segbuf + (size_t)pl->nseg_total * gq * p->cfg.head_dim;
-    dv.nwarps = p->num_sms * pl->k2_warps;
+    dv.nwarps = k2_sms(p) * pl->k2_warps;
     dv.k2_warps = pl->k2_warps;
     dv.ntiles = (int32_t)pl->tiles.size();
     dv.nreq = nreq;

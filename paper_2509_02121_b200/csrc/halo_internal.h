@@ -80,10 +80,12 @@ struct PoolGeom {
 
 // ---- launchers (kernels_*.cu) ----
 // K1: tcgen05/TMEM prefix attention -> normalised fp32 partials + lse (natural log).
+// tmap_q (nullable): 3-D map {d, q head, request} of q with box {64, g, 128/g}, 128-B
+// swizzle -- tiles whose requests are consecutive load their Q rows with it (TMA).
 cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v,
                                const CUtensorMap *tmap_k8, const CUtensorMap *tmap_v8,
-                               const PlanDev &p, const PoolGeom &g, int layer,
-                               const void *q, float scale, cudaStream_t s);
+                               const CUtensorMap *tmap_q, const PlanDev &p, const PoolGeom &g,
+                               int layer, const void *q, float scale, cudaStream_t s);
 // K2+K3: paged-suffix decode with the fused log-sum-exp merge of the K1 partials.
 cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void *pool_k,
                                  const void *pool_v, int layer, const void *q, float *out,

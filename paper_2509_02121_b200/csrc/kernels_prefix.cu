@@ -72,6 +72,7 @@ struct PrefixArgs {
     int32_t hq, hkv, g;
     int64_t layer_blk;  // layer * cap (4th TMA coordinate offset)
     float qscale;       // scale * log2(e)
+    int32_t tma_q;      // tmq is valid: tiles with consecutive requests load Q by TMA
 };
 
 template <int D>
@@ -111,7 +112,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                    const __grid_constant__ CUtensorMap tmk8, const __grid_constant__ CUtensorMap tmv8,
-                   const PrefixArgs a) {
+                   const __grid_constant__ CUtensorMap tmq, const PrefixArgs a) {
     using C = L1<D>;
     constexpr int SK = C::SK, SV = C::SV;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -129,11 +130,15 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     const int4 aux = a.p.tile_aux[blockIdx.x];  // loaded alongside T (no dependency)
     const int NT = (T.tok_end - T.tok_begin + kK1Tok - 1) / kK1Tok;
     const bool hasB = T.nrows > kSubRows;
+    // Q by TMA when the tile's requests are consecutive caller indices: one 3-D box
+    // {64 d, g heads, 128/g requests} per sub-tile and d atom lands rows request-major, head
+    // minor = the tile's row order, in the same 128-B swizzle the MMA descriptors expect
+    const bool tma_q = a.tma_q && aux.x >= 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         for (int x = 0; x < 2; ++x) {
-            ptx::mbar_init(&bar[Q_FULL + x], kSubRows);
+            ptx::mbar_init(&bar[Q_FULL + x], tma_q ? 1 : kSubRows);
             ptx::mbar_init(&bar[S_FULL + x], 1);
             ptx::mbar_init(&bar[P_FULL + x], kSubRows);
             ptx::mbar_init(&bar[PV_DONE + x], 1);
@@ -155,6 +160,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) K1_TRACE(9, 3);  // barriers + TMEM allocated
 
     // register split (setmaxnreg, per warpgroup): the softmax warpgroups hold a full
     // 128-column score row per thread; the producer / MMA / converter warpgroup gives back
@@ -172,14 +178,27 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             for (int i = lane; i < nblk; i += 32) blocks[i] = a.p.node_blocks[T.blk_off + blk_first + i];
         }
         __syncwarp();
-        // PDL: this grid may start while the previous kernel drains; the pool blocks it reads
-        // may have been written by that kernel (a registration or append), so wait here
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (lane == 0) {
+        if (lane == 0) {  // descriptors are kernel parameters: fetch them before the wait
             ptx::prefetch_tmap(&tmk);
             ptx::prefetch_tmap(&tmv);
             ptx::prefetch_tmap(&tmk8);
             ptx::prefetch_tmap(&tmv8);
+            if (tma_q) ptx::prefetch_tmap(&tmq);
+        }
+        // PDL: this grid may start while the previous kernel drains; the pool blocks it reads
+        // may have been written by that kernel (a registration or append), so wait here
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0) K1_TRACE(9, 4);  // producer: previous grid complete
+        if (lane == 0) {
+            if (tma_q) {
+                const int rq = kSubRows / a.g;  // requests per sub-tile
+                for (int x = 0; x < (hasB ? 2 : 1); ++x) {
+                    ptx::mbar_arrive_expect_tx(&bar[Q_FULL + x], C::Q_BYTES);
+                    for (int at = 0; at < C::ATOMS; ++at)
+                        ptx::tma_load_3d(sm + C::OFF_Q + x * C::Q_BYTES + at * C::ATOM_BYTES, &tmq, at * 64,
+                                         T.kv_head * a.g, aux.x + x * rq, &bar[Q_FULL + x]);
+                }
+            }
             auto issue = [&](const CUtensorMap *map, const CUtensorMap *map8, uint8_t *dst, uint64_t *full, int n) {
                 const int tok0 = T.tok_begin + n * kK1Tok;
                 const int nb = (min(kK1Tok, T.tok_end - tok0) + kBlockTok - 1) / kBlockTok;
@@ -314,7 +333,8 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         // Q row -> smem, K-major SW128 (16-B chunk c of row r lands at chunk c ^ (r & 7)).
         // q and the partials (read by the previous layer's K2) belong to earlier kernels.
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        {
+        if (threadIdx.x == 0) K1_TRACE(9, 5);  // softmax: previous grid complete, q load starts
+        if (!tma_q) {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.q + ((int64_t)req * a.hq + head) * D);
             uint8_t *qs = sm + C::OFF_Q + x * C::Q_BYTES;
 #pragma unroll
@@ -472,7 +492,7 @@ done:
 
 template <int D>
 cudaError_t launch_t(const CUtensorMap *tmk, const CUtensorMap *tmv, const CUtensorMap *tmk8,
-                     const CUtensorMap *tmv8, const PrefixArgs &a, cudaStream_t s) {
+                     const CUtensorMap *tmv8, const CUtensorMap *tmq, const PrefixArgs &a, cudaStream_t s) {
     auto kern = prefix_attn_kernel<D>;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -494,15 +514,15 @@ cudaError_t launch_t(const CUtensorMap *tmk, const CUtensorMap *tmv, const CUten
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, *tmk, *tmv, *tmk8, *tmv8, a);
+    return cudaLaunchKernelEx(&cfg, kern, *tmk, *tmv, *tmk8, *tmv8, *tmq, a);
 }
 
 }  // namespace
 
 cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v,
                                const CUtensorMap *tmap_k8, const CUtensorMap *tmap_v8,
-                               const PlanDev &p, const PoolGeom &g, int layer, const void *q,
-                               float scale, cudaStream_t s) {
+                               const CUtensorMap *tmap_q, const PlanDev &p, const PoolGeom &g,
+                               int layer, const void *q, float scale, cudaStream_t s) {
     if (p.ntiles == 0) return cudaSuccess;
     PrefixArgs a;
     a.p = p;
@@ -512,8 +532,10 @@ cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tma
     a.g = g.hq / g.hkv;
     a.layer_blk = (int64_t)layer * g.cap;
     a.qscale = scale * kLog2e;
-    if (g.d == 128) return launch_t<128>(tmap_k, tmap_v, tmap_k8, tmap_v8, a, s);
-    if (g.d == 64) return launch_t<64>(tmap_k, tmap_v, tmap_k8, tmap_v8, a, s);
+    a.tma_q = tmap_q != nullptr ? 1 : 0;
+    const CUtensorMap *tq = tmap_q != nullptr ? tmap_q : tmap_k;  // unused when tma_q == 0
+    if (g.d == 128) return launch_t<128>(tmap_k, tmap_v, tmap_k8, tmap_v8, tq, a, s);
+    if (g.d == 64) return launch_t<64>(tmap_k, tmap_v, tmap_k8, tmap_v8, tq, a, s);
     return cudaErrorInvalidValue;
 }
 

@@ -288,6 +288,31 @@ halo_status make_tmap(halo_pool p, void *base, CUtensorMap *out, int box_blocks)
     return HALO_OK;
 }
 
+// K1's Q map: q bf16 [nreq][hq][d] as dims {d, hq, nreq}; box {64, g, 128/g} = one
+// 128-row sub-tile (rows = request-major, q head of the kv group minor) per 64-wide d atom.
+halo_status make_qmap(halo_pool p, const void *q, int32_t nreq, CUtensorMap *out) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult qr;
+        void *f = nullptr;
+        HALO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr));
+        if (!f || qr != cudaDriverEntryPointSuccess)
+            return fail(HALO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)f;
+    }
+    const auto &c = p->cfg;
+    const int g = c.num_q_heads / c.num_kv_heads;
+    cuuint64_t dims[3] = {(cuuint64_t)c.head_dim, (cuuint64_t)c.num_q_heads, (cuuint64_t)nreq};
+    cuuint64_t strides[2] = {(cuuint64_t)c.head_dim * 2, (cuuint64_t)c.num_q_heads * c.head_dim * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(128 / g)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(q), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HALO_ECUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
+    return HALO_OK;
+}
+
 // ---------------------------------------------------------------- plan builder
 struct PNode {
     int64_t id;
@@ -962,7 +987,17 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
         return fail(HALO_EBUSY, "stale plan: a prefix node was offloaded or fetched since it was built");
     cudaError_t e;
     if (mask & 1) {
-        e = launch_prefix_attn(&p->tmap_k, &p->tmap_v, &p->tmap_k8, &p->tmap_v8, pl->dev, p->geom, layer, q, scale, s);
+        const CUtensorMap *tq = nullptr;
+        if (pl->dev.ntiles > 0 && pl->nreq > 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+            if (pl->tmap_q_ptr != q || pl->tmap_q_nreq != pl->nreq) {
+                pl->tmap_q_ok = make_qmap(p, q, pl->nreq, &pl->tmap_q) == HALO_OK;
+                pl->tmap_q_ptr = q;
+                pl->tmap_q_nreq = pl->nreq;
+            }
+            if (pl->tmap_q_ok) tq = &pl->tmap_q;
+        }
+        e = launch_prefix_attn(&p->tmap_k, &p->tmap_v, &p->tmap_k8, &p->tmap_v8, tq, pl->dev, p->geom, layer, q,
+                               scale, s);
         if (e != cudaSuccess) return fail(HALO_ECUDA, "prefix kernel launch: %s", cudaGetErrorString(e));
     }
     if (mask & 2) {

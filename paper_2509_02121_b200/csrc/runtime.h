@@ -157,6 +157,11 @@ struct halo_plan_s {
     size_t seg_cap = 0;
     int32_t *counters = nullptr;
     size_t counter_cap = 0;
+    // K1's TMA map of the q rows (encoded per q buffer; reused while q and nreq are unchanged)
+    CUtensorMap tmap_q{};
+    const void *tmap_q_ptr = nullptr;
+    int32_t tmap_q_nreq = -1;
+    bool tmap_q_ok = false;
     halo::PlanDev dev{};
     // staging for halo_decode_layers with host buffers
     void *q_stage = nullptr;

@@ -42,7 +42,10 @@ def main():
     t = buf.view(16, 64).cpu()
     t0 = int(t[9, 0])
     print("tile0 info:", plan.export("tiles")[0].tolist())
-    print(f"q loaded {(int(t[9,2])-t0)/1e3:.2f} us, epilogue done {(int(t[9,1])-t0)/1e3:.2f} us")
+    def at(e, n):
+        return f"{(int(t[e, n]) - t0) / 1e3:.2f} us" if int(t[e, n]) else "- (TMA)"
+    print(f"tmem+barriers {at(9, 3)}, producer past wait {at(9, 4)}, softmax past wait {at(9, 5)}, "
+          f"q loaded by the softmax threads {at(9, 2)}, epilogue done {at(9, 1)}")
     nt = int((t[2] > 0).sum())
     evs = [e for e in range(len(EV)) if EV[e]]
     print("tile " + " ".join(f"{EV[e]:>12s}" for e in evs))

@@ -37,6 +37,10 @@
 
 #include <cstdlib>
 
+#ifndef HALO_K1_PP_WARP
+#define HALO_K1_PP_WARP 1
+#endif
+
 #ifdef HALO_K1_TRACE
 // Debug timeline of CTA 0: g_k1_trace[event * 64 + tile] = %globaltimer (ns).
 __device__ unsigned long long *g_k1_trace = nullptr;  // [16][64]
@@ -87,7 +91,7 @@ struct L1 {
     static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
     static constexpr int OFF_V = OFF_K + SK * KV_BYTES;
     static constexpr int OFF_BAR = OFF_V + SV * KV_BYTES;
-    static constexpr int NBAR = 32;
+    static constexpr int NBAR = 40;
     static constexpr int OFF_BLK = OFF_BAR + NBAR * 8 + 16;       // block ids of the tile range
     static constexpr int MAX_BLK = kK1MaxTileTok / kBlockTok;
     static constexpr int SMEM = OFF_BLK + MAX_BLK * 4;              // base must be 1024-aligned
@@ -104,7 +108,8 @@ enum Bar {
     S_FULL = 2, P_FULL = 4, PV_DONE = 6,         // x2
     K_FULL = 8, K_EMPTY = 12,                    // x SK (<= 4)
     V_FULL = 16, V_EMPTY = 20, V_CONV = 24,      // x SV (<= 4)
-    EXP_DONE = 28                                // x2: sub-tile x finished its exp pass
+    EXP_DONE = 28,                               // x8: warp (x, w) of sub-tile x finished its exp
+                                                 // pass; index EXP_DONE + 4 x + w (w = warp & 3)
 
 };
 
@@ -142,7 +147,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             ptx::mbar_init(&bar[S_FULL + x], 1);
             ptx::mbar_init(&bar[P_FULL + x], kSubRows);
             ptx::mbar_init(&bar[PV_DONE + x], 1);
-            ptx::mbar_init(&bar[EXP_DONE + x], kSubRows);
+            for (int w = 0; w < 4; ++w) ptx::mbar_init(&bar[EXP_DONE + 4 * x + w], 32);
         }
         for (int s = 0; s < SK; ++s) {
             ptx::mbar_init(&bar[K_FULL + s], 1);
@@ -404,8 +409,14 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             // A's exp pass of tile n follows B's of tile n-1 and B's follows A's of tile n, so
             // one warpgroup's exponentials overlap the other's MMAs
             if (hasB) {
-                if (x == 1) ptx::mbar_wait(&bar[EXP_DONE + 0], n & 1);
-                else if (n >= 1) ptx::mbar_wait(&bar[EXP_DONE + 1], (n - 1) & 1);
+                // per SMSP: warp w of A pairs with warp w + 4 of B (same scheduler, same MUFU)
+#if HALO_K1_PP_WARP
+                if (x == 1) ptx::mbar_wait(&bar[EXP_DONE + wq], n & 1);
+                else if (n >= 1) ptx::mbar_wait(&bar[EXP_DONE + 4 + wq], (n - 1) & 1);
+#else
+                if (x == 1) for (int w = 0; w < 4; ++w) ptx::mbar_wait(&bar[EXP_DONE + w], n & 1);
+                else if (n >= 1) for (int w = 0; w < 4; ++w) ptx::mbar_wait(&bar[EXP_DONE + 4 + w], (n - 1) & 1);
+#endif
             }
             if (threadIdx.x == 0) K1_TRACE(7, n);
             const float2 c2v = make_float2(c2, c2), nm = make_float2(-m_ref, -m_ref);
@@ -434,7 +445,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             }
             const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
             l += (a01.x + a01.y) + (a23.x + a23.y);
-            if (hasB) ptx::mbar_arrive(&bar[EXP_DONE + x]);
+            if (hasB) ptx::mbar_arrive(&bar[EXP_DONE + 4 * x + wq]);
             if (threadIdx.x == 0) K1_TRACE(11, n);
             if (threadIdx.x == 128) K1_TRACE(13, n);
             ptx::tmem_wait_st();

@@ -153,6 +153,32 @@ def test_request_permutation_and_rerun_are_bit_identical():
     cleanup(ld, plan)
 
 
+@pytest.mark.parametrize("hq,hkv,d,per", [(32, 8, 128, 70), (8, 8, 64, 150), (16, 2, 128, 37),
+                                          (4, 2, 64, 70)])
+def test_k1_q_by_tma_equals_manual_q_load(hq, hkv, d, per):
+    """K1 loads a tile's Q rows by TMA when its requests are consecutive caller indices
+    (box {64, g, 128/g}, rows request-major), else thread by thread.  Two templates: in
+    template order every tile takes the TMA path (with a partial second sub-tile and, for
+    the last template, rows past the last request, zero-filled out of bounds); with the two
+    templates' requests interleaved no tile's requests are consecutive, so every tile loads
+    Q thread by thread.  Both land the same bytes in shared memory: the rows are
+    bit-identical, and match the oracle."""
+    wl = make_config("analytics", layers=1, templates=2, ctx=300, per_template=per, suffix=9,
+                     hq=hq, hkv=hkv, d=d)
+    ld, plan, out, lse = run_step(wl, opts(min_rows=1))
+    assert plan.info()["k1_tiles"] > 0
+    cleanup(ld, plan)
+    ro, rl = oracle.decode_reference(wl, 0, steps=1)
+    assert np.abs(out[0] - ro).max() <= OUT_TOL and np.abs(lse[0] - rl).max() <= LSE_TOL
+    inter = [i for pair in zip(range(per), range(per, 2 * per)) for i in pair]
+    ld, plan, outp, lsep = run_step(wl, opts(min_rows=1), reqs_perm=inter)
+    tiles = plan.export("tiles").reshape(-1, 8)
+    order = plan.export("req_order")
+    assert all(order[t[0] + 1] != order[t[0]] + 1 for t in tiles if t[1] > hq // hkv)  # manual path
+    cleanup(ld, plan)
+    assert np.array_equal(outp, out[:, inter]) and np.array_equal(lsep, lse[:, inter])
+
+
 def test_physical_block_placement_is_bit_invisible():
     wl = make_config("tree", layers=1, root=300, roles=3, role_tok=100, per_role=30, suffix=40)
     ld, plan, out, lse = run_step(wl)

@@ -37,10 +37,6 @@
 
 #include <cstdlib>
 
-#ifndef HALO_K1_PP_WARP
-#define HALO_K1_PP_WARP 1
-#endif
-
 #ifdef HALO_K1_TRACE
 // Debug timeline of CTA 0: g_k1_trace[event * 64 + tile] = %globaltimer (ns).
 __device__ unsigned long long *g_k1_trace = nullptr;  // [16][64]
@@ -410,13 +406,8 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             // one warpgroup's exponentials overlap the other's MMAs
             if (hasB) {
                 // per SMSP: warp w of A pairs with warp w + 4 of B (same scheduler, same MUFU)
-#if HALO_K1_PP_WARP
                 if (x == 1) ptx::mbar_wait(&bar[EXP_DONE + wq], n & 1);
                 else if (n >= 1) ptx::mbar_wait(&bar[EXP_DONE + 4 + wq], (n - 1) & 1);
-#else
-                if (x == 1) for (int w = 0; w < 4; ++w) ptx::mbar_wait(&bar[EXP_DONE + w], n & 1);
-                else if (n >= 1) for (int w = 0; w < 4; ++w) ptx::mbar_wait(&bar[EXP_DONE + 4 + w], (n - 1) & 1);
-#endif
             }
             if (threadIdx.x == 0) K1_TRACE(7, n);
             const float2 c2v = make_float2(c2, c2), nm = make_float2(-m_ref, -m_ref);

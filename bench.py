@@ -307,6 +307,38 @@ def measure_other_configs(halo, names, layers, steps, warmup, world, dev, torch,
     return res
 
 
+def measure_strong_scaling(halo, layers, steps, warmup, world, rank, dev, torch, dist):
+    """C2 (consolidated agent-DAG tree: 4k root -> 16 roles x 1k -> 1024 requests) with the
+    8 kv heads split 8/N per rank: every rank runs the same plan on its head slice (no
+    exchange step), so the total work is fixed as N grows.  Headline-pass timing (K1 -> K2
+    with PDL, the plan built once), max over ranks; queries/s = 1024 requests x layers /
+    time of the layers."""
+    from paper_2509_02121_b200.sharding import head_range, head_shard_workload
+    from synth import make_config
+    full = make_config("tree", layers=layers)
+    wl = head_shard_workload(full, world, rank)
+    ld, plan, info, step, bufs = setup_workload(halo, wl, dev, torch)
+    q, out, lse = bufs[2], bufs[3], bufs[4]
+
+    def layers(evs=None):  # the layers only: with 4 layers the per-step host plan would dominate
+        for l in range(wl.layers):
+            plan.run(l, q[l], out[l], lse[l])
+    ms, _, _, _, _ = time_steps(layers, wl.layers, steps, warmup, world, dev, torch, dist)
+    ms /= steps
+    lo, hi = head_range(full.hkv, world, rank)
+    res = {"workload": f"C2 tree, 1024 requests, kv heads sharded {full.hkv // world} per GPU "
+                       f"(total work fixed as N grows), {layers} layers",
+           "value": full.nreq * wl.layers / (ms * 1e-3), "unit": "queries/s",
+           "ms_per_step": ms, "n_gpus": world, "kv_heads_per_gpu": hi - lo,
+           "scaling": "strong"}
+    plan.destroy()
+    ld.pool.destroy()
+    del bufs, step
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -425,6 +457,10 @@ def main():
         guarded("other_configs", lambda: measure_other_configs(
             halo, [x for x in args.other_configs.split(",") if x], args.other_layers,
             max(3, min(args.steps, 10)), 3, world, dev, torch, dist))
+    # ---- strong scaling: C2 with its kv heads sharded over the ranks ----
+    if args.other_configs and not args.profile:
+        guarded("strong_scaling", lambda: measure_strong_scaling(
+            halo, args.other_layers, max(3, min(args.steps, 10)), 3, world, rank, dev, torch, dist))
     # ---- CPU oracle baseline ----
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         n, t, cores = oracle_sample(wl, args.cpu_budget)

@@ -320,9 +320,18 @@ def measure_strong_scaling(halo, layers, steps, warmup, world, rank, dev, torch,
     ld, plan, info, step, bufs = setup_workload(halo, wl, dev, torch)
     q, out, lse = bufs[2], bufs[3], bufs[4]
 
+    stream = torch.cuda.current_stream()
+
     def layers(evs=None):  # the layers only: with 4 layers the per-step host plan would dominate
         for l in range(wl.layers):
-            plan.run(l, q[l], out[l], lse[l])
+            if evs is None:
+                plan.run(l, q[l], out[l], lse[l])
+                continue
+            evs[l][0].record(stream)
+            plan.run_stages(l, 1, q[l], out[l], lse[l])
+            evs[l][1].record(stream)
+            plan.run_stages(l, 2, q[l], out[l], lse[l])
+            evs[l][2].record(stream)
     ms, _, _, _, _ = time_steps(layers, wl.layers, steps, warmup, world, dev, torch, dist)
     ms /= steps
     lo, hi = head_range(full.hkv, world, rank)
@@ -428,8 +437,9 @@ def main():
         extra["e2e"] = {"value": R * L * world * e2e_steps / dt, "unit": UNIT,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "steps": e2e_steps, "how": "halo_decode_step (append one token per request + "
-                        "plan + all layers; per-layer H2D/D2H on library copy streams overlapped "
-                        "with the kernels) with pinned host buffers; wall clock after sync"}
+                        "plan + all layers; H2D in 4-layer and D2H in 2-layer chunks on library "
+                        "copy streams, overlapped with the kernels) with pinned host buffers; "
+                        "wall clock after sync"}
     def guarded(key, fn):
         """The secondary legs must not cost the headline line: a failure is reported in place."""
         try:

@@ -1786,23 +1786,29 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
         memcpy(hs, w.slots.data(), w.slots.size() * 4);
         HALO_CUDA(pl->pin_slots.commit(pl->slot_stage, w.slots.size() * 4, s));
     }
-    // 3. per-layer pipeline: H2D (k, v, q of layer l) on the h2d stream | K5 append + K1 +
-    //    K2/K3 of layer l on `stream` | D2H (out of layer l) on the d2h stream.  The staging
+    // 3. pipeline: H2D (k, v, q) on the h2d stream in chunks of kH2DLayers layers, all issued
+    //    up front | K5 append + K1 + K2/K3 of layer l on `stream` (waits for its chunk) | D2H
+    //    (out, lse) on the d2h stream in chunks of kD2HLayers layers.  Chunk sizes measured on
+    //    B200 + PCIe host (tools/e2e_pipe_probe.py, C1): per-layer copies 4.0 ms/step, H2D x4 +
+    //    D2H x2 3.07 ms/step (both directions share ~89 GB/s; small D2H chunks start the
+    //    output stream early, larger H2D chunks cut the per-copy overhead).  The staging
     //    buffers are reused step to step: the copy streams first wait for `stream`.
+    constexpr int kH2DLayers = 4, kD2HLayers = 2;
     HALO_CUDA(cudaEventRecord(pl->ev_step, s));
     HALO_CUDA(cudaStreamWaitEvent(pl->h2d, pl->ev_step, 0));
     HALO_CUDA(cudaStreamWaitEvent(pl->d2h, pl->ev_step, 0));
     uint16_t *sk = static_cast<uint16_t *>(pl->kv_stage), *sv = sk ? sk + kv_layer * L : nullptr;
-    for (int l = 0; l < L; ++l) {
+    for (int l = 0; l < L; l += kH2DLayers) {
+        const int n = std::min(kH2DLayers, L - l);
         if (kv_host) {
             HALO_CUDA(cudaMemcpyAsync(sk + kv_layer * l, static_cast<const uint16_t *>(k_new) + kv_layer * l,
-                                      kv_layer * 2, cudaMemcpyHostToDevice, pl->h2d));
+                                      kv_layer * 2 * n, cudaMemcpyHostToDevice, pl->h2d));
             HALO_CUDA(cudaMemcpyAsync(sv + kv_layer * l, static_cast<const uint16_t *>(v_new) + kv_layer * l,
-                                      kv_layer * 2, cudaMemcpyHostToDevice, pl->h2d));
+                                      kv_layer * 2 * n, cudaMemcpyHostToDevice, pl->h2d));
         }
         if (q_host)
             HALO_CUDA(cudaMemcpyAsync(static_cast<uint16_t *>(pl->q_stage) + q_layer * l,
-                                      static_cast<const uint16_t *>(q) + q_layer * l, q_layer * 2,
+                                      static_cast<const uint16_t *>(q) + q_layer * l, q_layer * 2 * n,
                                       cudaMemcpyHostToDevice, pl->h2d));
         HALO_CUDA(cudaEventRecord(pl->ev_in[l], pl->h2d));
     }
@@ -1817,7 +1823,7 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
         if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
     }
     for (int l = 0; l < L; ++l) {
-        HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_in[l], 0));
+        if (l % kH2DLayers == 0) HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_in[l], 0));
         if (kv_host) {  // host K/V: append layer l once its copy has landed
             cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk + kv_layer * l, dv + kv_layer * l, nreq,
                                               pl->slot_stage, nreq, 0, l, l + 1, p->num_sms, s);
@@ -1825,14 +1831,16 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
         }
         st = run_layer(pl, l, dq + q_layer * l, dout + q_layer * l, dlse ? dlse + rows * l : nullptr, scale, s);
         if (st != HALO_OK) return st;
-        HALO_CUDA(cudaEventRecord(pl->ev_out[l], s));
-        if (o_host || l_host) {
+        if ((o_host || l_host) && (l % kD2HLayers == kD2HLayers - 1 || l == L - 1)) {
+            const int l0 = l - l % kD2HLayers, n = l - l0 + 1;
+            HALO_CUDA(cudaEventRecord(pl->ev_out[l], s));
             HALO_CUDA(cudaStreamWaitEvent(pl->d2h, pl->ev_out[l], 0));
             if (o_host)
-                HALO_CUDA(cudaMemcpyAsync(out + q_layer * l, dout + q_layer * l, q_layer * 4,
+                HALO_CUDA(cudaMemcpyAsync(out + q_layer * l0, dout + q_layer * l0, q_layer * 4 * n,
                                           cudaMemcpyDeviceToHost, pl->d2h));
             if (l_host)
-                HALO_CUDA(cudaMemcpyAsync(lse + rows * l, dlse + rows * l, rows * 4, cudaMemcpyDeviceToHost, pl->d2h));
+                HALO_CUDA(cudaMemcpyAsync(lse + rows * l0, dlse + rows * l0, rows * 4 * n, cudaMemcpyDeviceToHost,
+                                          pl->d2h));
         }
     }
     // the step is complete in `stream` order once the last download has landed

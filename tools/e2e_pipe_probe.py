@@ -44,6 +44,63 @@ def main():
                     dv[l].copy_(hv[l], non_blocking=True)
                     dq[l].copy_(hq[l], non_blocking=True)
                     ev_in[l].record(sa)
+        if mode.startswith("h"):  # hXdYpZ: H2D in X-layer chunks at most Z chunks ahead of
+            import re                # compute (0: all upfront), D2H in Y-layer chunks
+            X, Y, Z = map(int, re.match(r"h(\d+)d(\d+)p(\d+)", mode).groups())
+            nch = (L + X - 1) // X
+            ev_started = [torch.cuda.Event() for _ in range(nch)]
+
+            def h2d(c):
+                c0 = c * X
+                with torch.cuda.stream(sa):
+                    if Z > 0 and c - Z >= 0:
+                        sa.wait_event(ev_started[c - Z])
+                    dk[c0:c0 + X].copy_(hk[c0:c0 + X], non_blocking=True)
+                    dv[c0:c0 + X].copy_(hv[c0:c0 + X], non_blocking=True)
+                    dq[c0:c0 + X].copy_(hq[c0:c0 + X], non_blocking=True)
+                    ev_in[c0].record(sa)
+            for c in range(nch if Z == 0 else min(Z, nch)):
+                h2d(c)
+            for l in range(L):
+                if l % X == 0:
+                    s.wait_event(ev_in[l])
+                    c = l // X
+                    ev_started[c].record(s)
+                    if Z > 0 and c + Z < nch:
+                        h2d(c + Z)
+                plan.run(l, dq[l], out[l])
+                if l % Y == Y - 1 or l == L - 1:
+                    ev_out[l].record(s)
+                    c0 = l - l % Y
+                    with torch.cuda.stream(sb):
+                        sb.wait_event(ev_out[l])
+                        ho[c0:l + 1].copy_(out[c0:l + 1], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(sb)
+            s.wait_event(done)
+            return
+        if mode.startswith("chunk"):  # copies grouped G layers at a time, both directions
+            G = int(mode[5:])
+            with torch.cuda.stream(sa):
+                for c0 in range(0, L, G):
+                    dk[c0:c0 + G].copy_(hk[c0:c0 + G], non_blocking=True)
+                    dv[c0:c0 + G].copy_(hv[c0:c0 + G], non_blocking=True)
+                    dq[c0:c0 + G].copy_(hq[c0:c0 + G], non_blocking=True)
+                    ev_in[c0].record(sa)
+            for l in range(L):
+                if l % G == 0:
+                    s.wait_event(ev_in[l])
+                plan.run(l, dq[l], out[l])
+                if l % G == G - 1 or l == L - 1:
+                    ev_out[l].record(s)
+                    c0 = l - l % G
+                    with torch.cuda.stream(sb):
+                        sb.wait_event(ev_out[l])
+                        ho[c0:l + 1].copy_(out[c0:l + 1], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(sb)
+            s.wait_event(done)
+            return
         for l in range(L):
             if mode == "jit":
                 with torch.cuda.stream(sa):
@@ -72,7 +129,8 @@ def main():
         done.record(sb)
         s.wait_event(done)
 
-    for mode in ("none", "outonly", "upfront-noout", "upfront", "jit"):
+    modes = sys.argv[1:] or ["none", "outonly", "upfront-noout", "upfront", "jit", "chunk2", "chunk4", "chunk8"]
+    for mode in modes:
         for _ in range(3):
             step(mode)
         torch.cuda.synchronize()

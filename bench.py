@@ -322,7 +322,7 @@ def measure_strong_scaling(halo, layers, steps, warmup, world, rank, dev, torch,
 
     stream = torch.cuda.current_stream()
 
-    def layers(evs=None):  # the layers only: with 4 layers the per-step host plan would dominate
+    def run_layers(evs=None):  # the layers only: with 4 layers the per-step host plan would dominate
         for l in range(wl.layers):
             if evs is None:
                 plan.run(l, q[l], out[l], lse[l])
@@ -332,7 +332,7 @@ def measure_strong_scaling(halo, layers, steps, warmup, world, rank, dev, torch,
             evs[l][1].record(stream)
             plan.run_stages(l, 2, q[l], out[l], lse[l])
             evs[l][2].record(stream)
-    ms, _, _, _, _ = time_steps(layers, wl.layers, steps, warmup, world, dev, torch, dist)
+    ms, _, _, _, _ = time_steps(run_layers, wl.layers, steps, warmup, world, dev, torch, dist)
     ms /= steps
     lo, hi = head_range(full.hkv, world, rank)
     res = {"workload": f"C2 tree, 1024 requests, kv heads sharded {full.hkv // world} per GPU "
@@ -576,6 +576,8 @@ def measure_continuous(halo, wl, dev, torch, steps, churn=0.125):
     out = torch.empty((L, R, wl.hq, wl.d), device=f"cuda:{dev}")
     reqs = list(ld.req_ids)
     k_turn = max(1, int(R * churn))
+    # the joiners' prompt K/V as a prefill would leave it (built once, outside the timing)
+    skr, svr = sk.repeat(1, k_turn, 1, 1), sv.repeat(1, k_turn, 1, 1)
     plan = None
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -588,7 +590,7 @@ def measure_continuous(halo, wl, dev, torch, steps, churn=0.125):
             pool.close_request(reqs[j % R])
             reqs[j % R] = pool.open_request(tmpl)
         joined = [reqs[j % R] for j in range(lo, lo + k_turn)]
-        pool.append(joined, [S] * k_turn, sk.repeat(1, k_turn, 1, 1), sv.repeat(1, k_turn, 1, 1))
+        pool.append(joined, [S] * k_turn, skr, svr)
         plan = pool.decode_step(reqs, nk, nv, q, out, reuse=plan)
     e1.record(stream)
     torch.cuda.synchronize()

@@ -305,11 +305,12 @@ def _decode_step_outputs(wl, host: bool):
     return ld, plan, o, l_
 
 
-@pytest.mark.parametrize("host", [True, False])
-def test_decode_step_pipelined_matches_oracle_and_run(host):
-    """halo_decode_step (append + plan + every layer, copies overlapped per layer) equals the
-    oracle and is bit-identical to append + plan + halo_decode_run."""
-    wl = make_config("ragged", layers=3)
+@pytest.mark.parametrize("host,layers", [(True, 3), (False, 3), (True, 9)])
+def test_decode_step_pipelined_matches_oracle_and_run(host, layers):
+    """halo_decode_step (append + plan + every layer; host copies in 4-layer H2D / 2-layer
+    D2H chunks overlapped with the kernels -- 9 layers leave partial chunks in both
+    directions) equals the oracle and is bit-identical to append + plan + halo_decode_run."""
+    wl = make_config("ragged", layers=layers)
     ld, plan, o, l_ = _decode_step_outputs(wl, host)
     for layer in range(wl.layers):
         ro, rl = oracle.decode_reference(wl, layer, steps=1)

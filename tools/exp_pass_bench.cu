@@ -41,6 +41,55 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
     return make_float2(__uint_as_float(bx), __uint_as_float(by));
 }
 
+__device__ __forceinline__ uint32_t ex2h2(uint32_t x) {
+    uint32_t y; asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x)); return y;
+}
+// fp32 acc + f16 (lo / hi half of w): mixed-precision FMA with a 1.0 multiplier
+__device__ __forceinline__ float acc_h_lo(uint32_t w, float acc) {
+    asm("{\n\t.reg .b16 lo, hi, one;\n\tmov.b32 {lo, hi}, %1;\n\tmov.b16 one, 0x3C00;\n\t"
+        "fma.rn.f32.f16 %0, lo, one, %0;\n\t}" : "+f"(acc) : "r"(w));
+    return acc;
+}
+__device__ __forceinline__ float acc_h_hi(uint32_t w, float acc) {
+    asm("{\n\t.reg .b16 lo, hi, one;\n\tmov.b32 {lo, hi}, %1;\n\tmov.b16 one, 0x3C00;\n\t"
+        "fma.rn.f32.f16 %0, hi, one, %0;\n\t}" : "+f"(acc) : "r"(w));
+    return acc;
+}
+
+// the f16x2 MUFU pass: fp32 argument -> f16x2 -> ex2.approx.f16x2 (P is already packed), row
+// sum in fp32 with mixed-precision FMAs
+__global__ void pass_h2_kernel(float *out, int iters, long long *cyc) {
+    float s[128];
+    for (int i = 0; i < 128; ++i) s[i] = -(threadIdx.x % 7) * 0.01f - i * 0.003f;
+    const float2 c2v = make_float2(1.3f, 1.3f), nm = make_float2(-0.5f, -0.5f);
+    float acc[8] = {};
+    uint32_t sink = 0;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float2 e = ffma2(make_float2(s[32 * k + 2 * i], s[32 * k + 2 * i + 1]), c2v, nm);
+                pk[i] = ex2h2(h2(e.x, e.y));
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                acc[(2 * i) & 7] = acc_h_lo(pk[i], acc[(2 * i) & 7]);
+                acc[(2 * i + 1) & 7] = acc_h_hi(pk[i], acc[(2 * i + 1) & 7]);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sink ^= pk[i];
+        }
+        s[it & 127] += 1e-7f;
+    }
+    long long t1 = clock64();
+    float a = 0; for (int i = 0; i < 8; ++i) a += acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = a + sink;
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
 template <int NPOLY, int VARIANT = 0>  // VARIANT 1: no F2FP, 2: no F2FP/FADD2, 3: MUFU only
 __global__ void pass_kernel(float *out, int iters, long long *cyc) {
     float s[128];
@@ -91,6 +140,7 @@ int main() {
         }
     };
     run(pass_kernel<0>, "mufu");
+    run(pass_h2_kernel, "mufu-f16x2");
     run(pass_kernel<0, 1>, "no-f2fp");
     run(pass_kernel<0, 2>, "no-f2fp-add");
     run(pass_kernel<4>, "poly 4/16");

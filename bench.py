@@ -244,13 +244,18 @@ def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=Fa
     clk = ClockSampler(dev) if sample_clocks else None
     if clk:
         clk.__enter__()
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]  # headline step edges
     for p in range(2):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t[2 * p].record(stream)
         for s in range(steps):
+            if p == 0:
+                marks[s].record(stream)
             step(evs[s] if p == 1 else None)
+        if p == 0:
+            marks[steps].record(stream)
         t[2 * p + 1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -258,6 +263,10 @@ def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=Fa
     if clk:
         clk.__exit__()
     ms, ms_bd = t[0].elapsed_time(t[1]), t[2].elapsed_time(t[3])
+    per_step = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(steps))
+    time_steps.step_stats = {"median": per_step[len(per_step) // 2],
+                             "p90": per_step[min(len(per_step) - 1, (9 * len(per_step)) // 10)],
+                             "min": per_step[0], "max": per_step[-1], "rank": "this rank (rank 0)"}
     k1_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st)
     k2_ms = sum(e[1].elapsed_time(e[2]) for st in evs for e in st)
     from paper_2509_02121_b200.sharding import max_over_ranks
@@ -397,6 +406,7 @@ def main():
     stream = torch.cuda.current_stream()
     ms, ms_bd, k1_ms, k2_ms, clk = time_steps(step, L, args.steps, args.warmup, world, dev, torch, dist,
                                        sample_clocks=True)
+    step_stats = dict(time_steps.step_stats)  # the headline pass (later legs re-time)
     launches = args.steps * (1 + 2 * L)
     ms_step = ms / args.steps
     value = R * L * world * args.steps / (ms / 1e3)
@@ -493,6 +503,7 @@ def main():
                        "k1_tiles": info["k1_tiles"], "k2_units": info["k2_units"]},
             "roofline": dict(k2_roof, traffic=traffic),
             "prefix_roofline": k1_roof,
+            "step_ms_distribution": step_stats,
             "step_breakdown_ms": {"pass": "breakdown pass (events around each kernel)",
                                   "step": ms_bd / args.steps, "k1": k1_ms / args.steps,
                                   "k2": k2_ms / args.steps,

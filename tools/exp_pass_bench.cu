@@ -82,11 +82,57 @@ __global__ void pass_h2_kernel(float *out, int iters, long long *cyc) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) sink ^= pk[i];
         }
-        s[it & 127] += 1e-7f;
+        s[0] += 1e-7f;
     }
     long long t1 = clock64();
     float a = 0; for (int i = 0; i < 8; ++i) a += acc[i];
     out[blockIdx.x * blockDim.x + threadIdx.x] = a + sink;
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
+// phases over the whole row: all FFMA2 (in place), then all MUFU (in place), then the
+// sums and packs -- MUFU issues back to back without waiting on the chunk tails
+template <int MAX3>
+__global__ void pass_phased_kernel(float *out, int iters, long long *cyc) {
+    float s[128];
+    for (int i = 0; i < 128; ++i) s[i] = -(threadIdx.x % 7) * 0.01f - i * 0.003f;
+    const float2 c2v = make_float2(1.3f, 1.3f), nm = make_float2(-0.5f, -0.5f);
+    float2 acc[4] = {};
+    uint32_t sink = 0;
+    float mxs = -1e30f;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        float *x = s;  // in place, as K1 can do with its score row
+        // row max (2- or 3-input max)
+        float m0 = s[0], m1 = s[1];
+        if (MAX3) {
+#pragma unroll
+            for (int i = 2; i + 3 < 128; i += 4) {
+                asm("max.f32 %0, %0, %1, %2;" : "+f"(m0) : "f"(s[i]), "f"(s[i + 1]));
+                asm("max.f32 %0, %0, %1, %2;" : "+f"(m1) : "f"(s[i + 2]), "f"(s[i + 3]));
+            }
+        } else {
+#pragma unroll
+            for (int i = 2; i + 1 < 128; i += 2) { m0 = fmaxf(m0, s[i]); m1 = fmaxf(m1, s[i + 1]); }
+        }
+        mxs = fmaxf(mxs, fmaxf(m0, m1));
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const float2 e = ffma2(make_float2(s[2 * i], s[2 * i + 1]), c2v, nm);
+            x[2 * i] = e.x; x[2 * i + 1] = e.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 128; ++i) x[i] = ex2(x[i]);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const float2 e = make_float2(x[2 * i], x[2 * i + 1]);
+            acc[i & 3] = fadd2(acc[i & 3], e);
+            sink ^= h2(e.x, e.y);
+        }
+        s[0] += 1e-7f;
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0].x + acc[1].y + acc[2].x + acc[3].y + sink + mxs;
     if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
 }
 
@@ -119,7 +165,7 @@ __global__ void pass_kernel(float *out, int iters, long long *cyc) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) sink ^= pk[i];
         }
-        s[it & 127] += 1e-7f;  // keep the loop honest
+        s[0] += 1e-7f;  // keep the loop honest (static index: s stays in registers)
     }
     long long t1 = clock64();
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0].x + acc[1].y + acc[2].x + acc[3].y + sink;
@@ -141,6 +187,8 @@ int main() {
     };
     run(pass_kernel<0>, "mufu");
     run(pass_h2_kernel, "mufu-f16x2");
+    run(pass_phased_kernel<0>, "phased+max");
+    run(pass_phased_kernel<1>, "phased+max3");
     run(pass_kernel<0, 1>, "no-f2fp");
     run(pass_kernel<0, 2>, "no-f2fp-add");
     run(pass_kernel<4>, "poly 4/16");

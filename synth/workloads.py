@@ -47,6 +47,10 @@ class Workload:
     requests: list
     seed: int = 0
     alpha_q: float = 1.0
+    # attention-sink variant (SURVEY.md §8(d) "sink (+8 on token 0 of the root)"): token 0
+    # of every root node gets the key K0 * e_0 and every query gets +SINK_QB on dim 0, so its
+    # scaled score is sink * (1 + z * alpha / SINK_QB) with z ~ N(0,1): +sink on average.
+    sink: float = 0.0
     notes: dict = field(default_factory=dict)
 
     # ---- structure -------------------------------------------------------------------
@@ -85,9 +89,21 @@ class Workload:
     def _key(self, kind: str, ident: int) -> TensorKey:
         return TensorKey(self.seed, kind, ident)
 
+    SINK_QB = 4.0  # query bias on dim 0 of the sink variant
+
     def node_kv(self, n: int, device="cpu", layer=None):
         nt = self.node(n).ntok
-        return self._pair("node_k", "node_v", n, nt, self.hkv, device, layer)
+        k, v = self._pair("node_k", "node_v", n, nt, self.hkv, device, layer)
+        if self.sink > 0 and self.node(n).parent < 0:
+            # K0 = sink * sqrt(d) / SINK_QB on dim 0, zero elsewhere (exact in bf16 after rounding)
+            k0 = torch.zeros(self.hkv, self.d, dtype=torch.float32)
+            k0[:, 0] = self.sink * (self.d ** 0.5) / self.SINK_QB
+            k0 = k0.to(torch.bfloat16).to(k.device)
+            if layer is None:
+                k[:, 0] = k0
+            else:
+                k[0] = k0
+        return k, v
 
     def suffix_kv(self, device="cpu", layer=None, request=None):
         """Initial suffixes of all requests: [L][sum S][Hkv][d], or one request's slice."""
@@ -104,7 +120,10 @@ class Workload:
 
     def q(self, step: int, device="cpu", layer=None, request=None):
         """Decode queries of step `step`: [L][R][Hq][d] (or a slice)."""
-        return self._rows("q", step, self.hq, device, layer, request, self.alpha_q)
+        q = self._rows("q", step, self.hq, device, layer, request, self.alpha_q)
+        if self.sink > 0:  # + SINK_QB on dim 0, rounded to bf16 (same on CPU and GPU)
+            q[..., 0] = (q[..., 0].float() + self.SINK_QB).to(torch.bfloat16)
+        return q
 
     def new_kv(self, step: int, device="cpu", layer=None, request=None):
         """K/V of the token appended at step `step`: [L][R][Hkv][d] (or a slice)."""

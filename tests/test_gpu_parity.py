@@ -112,9 +112,19 @@ def test_ragged_suffix_lengths():
     check(make_config("ragged_suffix", layers=1, nreq=40, prefix=512))
 
 
-@pytest.mark.parametrize("alpha", [2.0])
+@pytest.mark.parametrize("alpha", [2.0, 4.0, 8.0])
 def test_sharper_scores(alpha):
+    """alpha = 2 and the stress alphas 4 / 8 (sharp, competing peaks; SURVEY.md §8(c) error
+    budget): gated at the same 2e-3, since K1's P is fp16 (the budget's fp16-P column)."""
     check(make_config("fanout", layers=1, nreq=64, prefix=600, suffix=30, alpha_q=alpha))
+
+
+@pytest.mark.parametrize("cfg,kw", [("fanout", dict(nreq=64, prefix=600, suffix=30)),
+                                    ("tree", dict(root=300, roles=3, role_tok=130, per_role=30, suffix=20))])
+def test_attention_sink(cfg, kw):
+    """Attention-sink variant (+8 on token 0 of every root): most of the
+    probability mass on one prefix token, in K1's first n-tile."""
+    check(make_config(cfg, layers=1, sink=8.0, **kw))
 
 
 def test_d64_g2():

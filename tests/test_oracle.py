@@ -293,3 +293,20 @@ def test_generator_is_device_independent_and_seeded():
     x = a.float()
     assert abs(float(x.mean())) < 0.15 and 0.9 < float(x.std()) < 1.4
     assert torch.equal((x * 32).round(), x * 32)  # multiples of 1/32: bf16-exact
+
+
+def test_sink_variant_inputs():
+    """The sink workload (inputs only): token 0 of a root carries K0 e_0 and every query has
+    +4 on dim 0, so token 0's scaled score averages +sink; other tokens stay centred; the
+    node tensors read per layer equal the all-layer read."""
+    wl = make_config("fanout", layers=2, nreq=16, prefix=40, suffix=3, sink=8.0)
+    k, _ = wl.node_kv(0, "cpu")
+    for layer in range(2):
+        kl, _ = wl.node_kv(0, "cpu", layer)
+        assert torch.equal(kl, k[layer])
+        q = wl.q(0, "cpu", layer).double()
+        s0 = torch.einsum("rhd,hd->rh", q, kl[0].double().repeat_interleave(wl.g, 0)) / wl.d ** 0.5
+        s5 = torch.einsum("rhd,hd->rh", q, kl[5].double().repeat_interleave(wl.g, 0)) / wl.d ** 0.5
+        assert abs(s0.mean().item() - 8.0) < 0.5 and abs(s5.mean().item()) < 0.5
+    assert float(k[0, 0, 0, 1]) == 0.0
+    assert abs(float(k[0, 0, 0, 0]) - 8.0 * wl.d ** 0.5 / wl.SINK_QB) < 0.1

@@ -137,13 +137,12 @@ def test_g8_and_g1():
           opts(min_rows=1))
 
 
-def test_full_c1_sampled_at_bench_configuration():
-    """C1 (BASELINE configs[1]) at full size: 256 requests, 2k prefix, 32 layers; sampled
-    requests at the first and last layer vs the oracle (the launch configuration bench.py
+def test_full_c1_at_bench_configuration():
+    """C1 (BASELINE configs[1]) at full size: 256 requests, 2k prefix, 32 layers; every
+    request at the first and last layer vs the oracle (the launch configuration bench.py
     times: default plan)."""
     wl = make_config("fanout")
-    sample = [0, 1, 77, 128, 200, 255]
-    check(wl, layers=[0, 31], sample=sample)
+    check(wl, layers=[0, 31])   # every request (SURVEY.md §8(c): C0-C2 all requests)
 
 
 def test_request_permutation_and_rerun_are_bit_identical():
@@ -351,17 +350,20 @@ def test_decode_step_reuses_its_plan_across_steps():
     cleanup(ld, plan)
 
 
-def test_full_c2_tree_sampled_at_bench_configuration():
+def test_full_c2_tree_at_bench_configuration():
     """C2 (BASELINE configs[2]): 4k root -> 16 x 1k roles -> 1024 requests, two prefix levels
     merged with the suffix; the per-layer shapes bench.py's other_configs leg times."""
     wl = make_config("tree", layers=2)
-    check(wl, layers=[1], sample=[0, 63, 64, 500, 1023])
+    check(wl, layers=[1])       # all 1024 requests
 
 
 def test_full_c3_analytics_sampled_at_bench_configuration():
     """C3 per GPU (BASELINE configs[3]): 8 templates x 8k-token contexts x 256 requests."""
     wl = make_config("analytics", layers=1)
-    check(wl, layers=[0], sample=[0, 255, 256, 1100, 2047])
+    # a seeded sample of 512 requests covering every template of the GPU (64 per template)
+    rng = np.random.Generator(np.random.PCG64(3))
+    sample = sorted(int(t * 256 + r) for t in range(8) for r in rng.choice(256, 64, replace=False))
+    check(wl, layers=[0], sample=sample)
 
 
 def test_continuous_batching_requests_join_and_leave_between_steps():

@@ -759,6 +759,35 @@ def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):
         torch.cuda.synchronize()
         dst.destroy()
         del kx, vx
+        # C4 shape on one GPU: nodes of 1k..32k tokens x 32 layers x 8 heads (128 MiB..4 GiB
+        # of K+V), K4 pack and same-GPU relocation GB/s vs node size
+        sweep = []
+        big = (32768 + 15) // 16
+        src = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, big + 16, dev)
+        dst = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, big + 16, dev)
+        for ntok in (1024, 2048, 4096, 8192, 16384, 32768):
+            kx = torch.empty((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
+            vx = torch.empty_like(kx)
+            kx.normal_()
+            vx.normal_()
+            nd = src.register_prefix(-1, ntok, kx, vx, stream)
+            nb = ntok * wl.layers * wl.hkv * wl.d * 2 * 2
+
+            def clone2():
+                n2 = src.clone_prefix(nd, dst, -1, stream)
+                dst.release_prefix(n2)
+            ms_c = timed(clone2)
+            ms_p = timed(lambda: src.read_prefix(nd, kx, vx, stream))
+            sweep.append({"tokens": ntok, "bytes": nb, "relocate_ms": ms_c,
+                          "relocate_hbm_frac": 2 * nb / ms_c / 1e6 / hbm_peak,
+                          "pack_ms": ms_p, "pack_hbm_frac": 2 * nb / ms_p / 1e6 / hbm_peak})
+            torch.cuda.synchronize()
+            src.release_prefix(nd)
+            del kx, vx
+        torch.cuda.synchronize()
+        src.destroy()
+        dst.destroy()
+        res["sweep"] = sweep
         return res
     uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
     obj = [uid]

@@ -374,6 +374,35 @@ int k2_sms(halo_pool p) {
     return (n > 0 && n < p->num_sms) ? n : p->num_sms;
 }
 
+// Experiment hook (HALO_K2_EARLY_W=x): weight of the K2 warps whose CTAs start on SMs that K1
+// leaves idle (blockIdx < num_sms - K1 CTAs) relative to those that enter as K1 retires.
+double k2_early_weight_env() {
+    static const double w = [] {
+        const char *e = getenv("HALO_K2_EARLY_W");
+        return e ? atof(e) : 1.2;
+    }();
+    return w;
+}
+
+// Experiment hook (HALO_K1_SM_FRAC=x, 0 disables): the fraction of the SMs a single-wave K1
+// may occupy when K2 dominates the layer (section 7 of the planner).
+double k1_sm_frac() {
+    static const double f = [] {
+        const char *e = getenv("HALO_K1_SM_FRAC");
+        return e ? atof(e) : 0.65;
+    }();
+    return f;
+}
+
+// Experiment hook (HALO_K2_FORCE_WIDE=1): always use K2's wide launch shape.
+bool force_wide() {
+    static const bool f = [] {
+        const char *e = getenv("HALO_K2_FORCE_WIDE");
+        return e && atoi(e) != 0;
+    }();
+    return f;
+}
+
 // Test hook (HALO_K2_FORCE_NARROW=1): always use K2's narrow launch shape.
 bool force_narrow() {
     static const bool f = [] {
@@ -516,7 +545,50 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             n.splits = (int)ceil_div(tok, n.chunk);
         }
     } else {
-        const int C = choose_chunk(ns, g, hkv, p->num_sms, max_splits);
+        int C = choose_chunk(ns, g, hkv, p->num_sms, max_splits);
+        // K1 in a single partial wave beside a K2 that dominates the layer: under programmatic
+        // dependent launch K2's first CTAs stream on the SMs K1 leaves idle, so fewer, longer
+        // K1 tiles (split count lowered until the tiles fit k1_sm_frac of the SMs) free SMs
+        // for K2 while K1 runs; K2's early CTAs then get a larger share (section 12b).  Applied
+        // only when K2's estimated time is at least 2.4x K1's at the lowered split count: below
+        // that, K2's early units wait for K1 at their merge (measured on 8 fan-out shapes,
+        // tools/k2_early_sweep3.sh: ratios 2.5-10 gain 3-8%, ratios ~2.1 lose 4-11%).
+        // (C1: 4 -> 3 splits, 128 -> 96 K1 CTAs, 3.59 -> 3.71 M queries/s; K2.)
+        pl->k2_early = false;
+        if (k1_sm_frac() > 0 && pl->opt.max_splits <= 0) {
+            auto tiles_for = [&](int64_t Cc, int64_t &max_ch) {
+                int64_t T = 0;
+                max_ch = 0;
+                for (auto &n : ns) {
+                    if (!n.tensor) continue;
+                    const int64_t tok = n.node->ntok;
+                    int64_t sp = std::max(std::min<int64_t>(ceil_div(tok, Cc), max_splits), ceil_div(tok, kK1MaxTileTok));
+                    const int64_t ch = ceil_div(ceil_div(tok, sp), kK1Tok) * kK1Tok;
+                    sp = ceil_div(tok, ch);
+                    T += ceil_div((int64_t)(n.r1 - n.r0) * g, kK1Rows) * hkv * sp;
+                    max_ch = std::max(max_ch, std::min(ch, tok));
+                }
+                return T;
+            };
+            int64_t mc = 0;
+            const int64_t T0 = tiles_for(C, mc);
+            double k2_bytes_est = 0;
+            for (int i = 0; i < nreq; ++i) k2_bytes_est += (double)R[i]->blocks.size() * kBlockTok * hkv * D * 4;
+            const double cap = k1_sm_frac() * p->num_sms;
+            if (T0 > 0 && T0 <= p->num_sms && (double)T0 > cap) {
+                for (int64_t Cc = C + kK1Tok; Cc <= kK1MaxTileTok; Cc += kK1Tok) {
+                    const int64_t T1 = tiles_for(Cc, mc);
+                    if ((double)T1 > cap) continue;
+                    const double t_k1_us = 3.5 + 2.4 * (double)ceil_div(mc, kK1Tok);  // measured per-CTA
+                    const double t_k2_us = k2_bytes_est / 6.0e6;                       // ~6 TB/s
+                    if (T1 > 0 && t_k2_us >= 2.4 * t_k1_us) {
+                        C = (int)Cc;
+                        pl->k2_early = true;
+                    }
+                    break;
+                }
+            }
+        }
         for (auto &n : ns) {
             if (!n.tensor) continue;
             const int64_t tok = n.node->ntok;
@@ -726,25 +798,43 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             }
             if (x > c.back() && x < Itot) c.push_back(x);
         };
-        auto equal_cuts = [&](int64_t nw) {
+        // Under programmatic dependent launch K2's CTAs are dispatched in blockIdx order: the
+        // first num_sms - (K1 CTAs) land on SMs K1 leaves idle and stream while K1 runs; the
+        // rest enter as K1's CTAs retire.  Warps of the early CTAs get `ew` times the share.
+        const int64_t k1c = (int64_t)pl->tiles.size();
+        const int64_t early_ctas = (k1c > 0 && k1c < k2_sms(p)) ? k2_sms(p) - k1c : 0;
+        const double ew = early_ctas > 0 && (pl->k2_early || getenv("HALO_K2_EARLY_W")) && k2_early_weight_env() > 0
+                              ? k2_early_weight_env() : 1.0;
+        auto target = [&](int64_t w, int64_t nw, int wpc) -> int64_t {  // item position of cut w
+            if (ew == 1.0) return w * Itot / nw;
+            const int64_t ne = std::min<int64_t>(nw, early_ctas * wpc);
+            const double tot = (double)ne * ew + (double)(nw - ne);
+            const double cw = (double)std::min<int64_t>(w, ne) * ew + (double)std::max<int64_t>(0, w - ne);
+            return (int64_t)(cw / tot * (double)Itot);
+        };
+        auto equal_cuts = [&](int64_t nw, int wpc) {
             std::vector<int64_t> c(1, 0);
-            for (int64_t w = 1; w < nw; ++w) push_cut(c, w * Itot / nw);
+            for (int64_t w = 1; w < nw; ++w) push_cut(c, target(w, nw, wpc));
             c.push_back(Itot);
             return c;
         };
         // cuts snapped to the nearest unit boundary; `balanced` if the largest chunk stays
         // within 5% of the equal share (whole units: no stream-K merges)
-        auto snapped_cuts = [&](int64_t nw, bool &balanced) {
+        auto snapped_cuts = [&](int64_t nw, int wpc, bool &balanced) {
             std::vector<int64_t> c(1, 0);
             for (int64_t w = 1; w < nw && Itot > 0; ++w) {
-                const int64_t x = w * Itot / nw, u = unit_of(x);
+                const int64_t x = target(w, nw, wpc), u = unit_of(x);
                 const int64_t y = (x - ui(u) <= ui(u + 1) - x) ? ui(u) : ui(u + 1);
                 if (y > c.back() && y < Itot) c.push_back(y);
             }
             c.push_back(Itot);
-            int64_t mx = 0;
-            for (size_t k = 1; k < c.size(); ++k) mx = std::max<int64_t>(mx, c[k] - c[k - 1]);
-            balanced = mx * 100 <= ceil_div(Itot, nw) * 105;
+            // largest chunk against its warp's (weighted) share
+            balanced = true;
+            for (size_t k = 1; k < c.size(); ++k) {
+                const int64_t w = (int64_t)k - 1;
+                const int64_t share = std::max<int64_t>(1, ceil_div(target(w + 1, nw, wpc) - target(w, nw, wpc), 1));
+                if ((c[k] - c[k - 1]) * 100 > std::max<int64_t>(share, ceil_div(Itot, nw)) * 105) balanced = false;
+            }
             return c;
         };
         std::vector<int64_t> cuts;
@@ -755,14 +845,16 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             cuts.push_back(Itot);
         } else if (force_narrow()) {  // test hook
             pl->k2_warps = kK2WarpsNarrow;
-            cuts = equal_cuts(Wn);
-        } else if (U < 2 * Ww && (cuts = snapped_cuts(Wn, bal), bal)) {
+            cuts = equal_cuts(Wn, kK2WarpsNarrow);
+        } else if (force_wide()) {  // experiment hook
+            cuts = equal_cuts(Ww, kK2WarpsWide);
+        } else if (U < 2 * Ww && (cuts = snapped_cuts(Wn, kK2WarpsNarrow, bal), bal)) {
             // few units per warp (stream-K pieces would dominate) and whole units divide
             // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
             pl->k2_warps = kK2WarpsNarrow;
         } else {
-            cuts = snapped_cuts(Ww, bal);
-            if (!bal) cuts = equal_cuts(Ww);  // equal item ranges (stream-K pieces)
+            cuts = snapped_cuts(Ww, kK2WarpsWide, bal);
+            if (!bal) cuts = equal_cuts(Ww, kK2WarpsWide);  // equal item ranges (stream-K pieces)
         }
         if (cuts.size() < 2) cuts = {0, Itot};
         const int64_t nchunks = (int64_t)cuts.size() - 1;

@@ -301,3 +301,46 @@ def test_k2_schedule_spreads_blockless_units_over_warps():
     assert np.all(cover == 1) and np.all(clo == 0)
     pl.destroy()
     p.destroy()
+
+
+def _k2_warp_blocks(pl, nwarps):
+    """Blocks of K2 work per warp (warp w takes chunk w when chunks <= warps)."""
+    clo = pl.export("chunk_lo")
+    sizes = np.diff(clo)
+    assert len(sizes) <= nwarps
+    return sizes
+
+
+def test_single_wave_k1_rule_lowers_splits_and_weights_early_k2_warps():
+    """Planner section 7: a single-wave K1 beside a K2 that dominates the layer gets fewer,
+    longer tiles (<= 0.65 x 148 CTAs), and the K2 warps of the CTAs that start on the SMs K1
+    leaves idle (blockIdx < 148 - K1 CTAs) get ~1.2x the blocks of the others (DESIGN.md,
+    "K2 beside a single-wave K1").  Shapes where K2 does not dominate keep the default split
+    choice, and an explicit split cap disables the rule."""
+    nsm, wide = 148, 12
+    # C1: 256 requests x 2048-token prefix + 256-token suffixes -> 96 tiles (3 splits)
+    wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=255)
+    p, ld, pl = plan_of(wl)
+    info = pl.info()
+    assert info["k1_tiles"] == 96
+    sizes = _k2_warp_blocks(pl, nsm * wide)
+    early = (nsm - 96) * wide
+    ratio = sizes[:early].mean() / sizes[early:].mean()
+    assert 1.1 <= ratio <= 1.3, ratio
+    assert sizes.sum() == 256 * 8 * 16  # every suffix block of every (request, kv head) once
+    pl.destroy(); p.destroy()
+    # small K2 (16-token suffixes): K1 keeps its default single wave of 128 tiles, equal shares
+    wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=15)
+    p, ld, pl = plan_of(wl)
+    assert pl.info()["k1_tiles"] == 128
+    pl.destroy(); p.destroy()
+    # K2 / K1 estimate ratio ~2.1 (128 requests): excluded by the 2.4x threshold
+    wl = make_config("fanout", layers=1, nreq=128, prefix=2048, suffix=255)
+    p, ld, pl = plan_of(wl)
+    assert pl.info()["k1_tiles"] == 128
+    pl.destroy(); p.destroy()
+    # explicit split cap: the rule is off
+    wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=255)
+    p, ld, pl = plan_of(wl, max_splits=4)
+    assert pl.info()["k1_tiles"] == 128
+    pl.destroy(); p.destroy()

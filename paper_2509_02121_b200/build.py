@@ -31,6 +31,10 @@ def build(verbose: bool = False, force: bool = False, extra: list[str] | None = 
     """Compile the sources into `lib` (default: the in-tree libhalo_attn.so).  `extra` nvcc
     flags + a different `lib`/`build_dir` give debug variants (e.g. -DHALO_K1_TRACE)."""
     BUILD_ = build_dir
+    if lib != LIB and build_dir == BUILD:
+        # a variant keeps its own objects: sharing them would let the next default build()
+        # relink libhalo_attn.so from the variant's (newer) objects
+        BUILD_ = BUILD + "_" + os.path.splitext(os.path.basename(lib))[0]
     os.makedirs(BUILD_, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "halo_attn.h")]
     objs, jobs = [], []

@@ -295,8 +295,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 const int64_t off = (int64_t)(ex & kBlkMask) * (kBlockTok * D);
                 uint8_t *dst = ws + st * S::STAGE;
                 ptx::mbar_arrive_expect_tx(&full[st], S::STAGE);
+#ifndef HALO_K2_NO_L2_HINT
+                // suffix K/V is read exactly once: an L2 evict_first policy keeps K1's
+                // partials, q and the plan resident in L2 (C1 3.75 -> 4.02 M queries/s)
+                const uint64_t pol = ptx::l2_policy_evict_first();
+                ptx::bulk_g2s_hint(dst, pk + off, S::SLAB, &full[st], pol);
+                ptx::bulk_g2s_hint(dst + S::SLAB, pv + off, S::SLAB, &full[st], pol);
+#else
                 ptx::bulk_g2s(dst, pk + off, S::SLAB, &full[st]);
                 ptx::bulk_g2s(dst + S::SLAB, pv + off, S::SLAB, &full[st]);
+#endif
             }
             ++px;
             ++p_count;

@@ -53,7 +53,8 @@ struct PlanDev {
     // chunk c visits units [chunk_u0[c], chunk_u1[c]).  A unit cut by chunk boundaries
     // writes nseg partial states (slots unit_seg..) merged by the last arriving piece.
     // k2_ent[x] describes global block x: {slab | (ntok-1) << 27 | unit start << 31,
-    // q group row}, slab = pool block * hkv + kv head, q group row = request * hkv + head.
+    // q group row | shared << 31}, slab = pool block * hkv + kv head, q group row =
+    // request * hkv + head, shared = the block belongs to a folded prefix node (L2 policy).
     // unit_meta[2u], [2u+1] = {boff_begin, boff_end, request, kv head},
     //                         {nslots, nseg, first seg slot, first chunk}.
     const uint2 *k2_ent;         // [nblocks]

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 if (lane == 0) {
                     const int qi = (int)(q_issued % S::QN);
                     ptx::mbar_arrive_expect_tx(&qbar[qi], S::QB);
-                    ptx::bulk_g2s(qbuf + qi * S::QB, a.q + (int64_t)ey * (G * D), S::QB, &qbar[qi]);
+                    ptx::bulk_g2s(qbuf + qi * S::QB, a.q + (int64_t)(ey & 0x7fffffffu) * (G * D), S::QB, &qbar[qi]);
                 }
                 ++q_issued;
             }
@@ -297,10 +297,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 ptx::mbar_arrive_expect_tx(&full[st], S::STAGE);
 #ifndef HALO_K2_NO_L2_HINT
                 // suffix K/V is read exactly once: an L2 evict_first policy keeps K1's
-                // partials, q and the plan resident in L2 (C1 3.75 -> 4.02 M queries/s)
-                const uint64_t pol = ptx::l2_policy_evict_first();
-                ptx::bulk_g2s_hint(dst, pk + off, S::SLAB, &full[st], pol);
-                ptx::bulk_g2s_hint(dst + S::SLAB, pv + off, S::SLAB, &full[st], pol);
+                // partials, q and the plan resident in L2 (C1 3.75 -> 4.02 M queries/s).
+                // Blocks of folded prefix nodes (bit 31 of the entry) are read by several
+                // units and keep the default policy.
+                if (ey >> 31) {
+                    ptx::bulk_g2s(dst, pk + off, S::SLAB, &full[st]);
+                    ptx::bulk_g2s(dst + S::SLAB, pv + off, S::SLAB, &full[st]);
+                } else {
+                    const uint64_t pol = ptx::l2_policy_evict_first();
+                    ptx::bulk_g2s_hint(dst, pk + off, S::SLAB, &full[st], pol);
+                    ptx::bulk_g2s_hint(dst + S::SLAB, pv + off, S::SLAB, &full[st], pol);
+                }
 #else
                 ptx::bulk_g2s(dst, pk + off, S::SLAB, &full[st]);
                 ptx::bulk_g2s(dst + S::SLAB, pv + off, S::SLAB, &full[st]);

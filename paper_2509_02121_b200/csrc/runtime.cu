@@ -394,6 +394,16 @@ double k1_sm_frac() {
     return f;
 }
 
+// Experiment hook (HALO_K2_SHARED_NORMAL=0): stream folded prefix-node blocks with
+// evict_first like the private suffix blocks.
+bool k2_shared_normal() {
+    static const bool v = [] {
+        const char *e = getenv("HALO_K2_SHARED_NORMAL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
 // Experiment hook (HALO_K2_FORCE_WIDE=1): always use K2's wide launch shape.
 bool force_wide() {
     static const bool f = [] {
@@ -742,8 +752,10 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     };
     int folded = 0;
     for (auto &n : ns) folded += !n.tensor;
+    std::vector<int32_t> req_fold_blk(nreq, 0);  // leading blocks of folded (shared) path nodes
     for (int i = 0; i < nreq; ++i) {
         pl->req_blk_off[i] = (int32_t)pl->req_blk.size();
+        const size_t fold0 = pl->req_blk.size();
         path.clear();
         for (int x = leaf_loc[i]; x >= 0; x = ns[x].parent) path.push_back(x);
         int64_t ctx = R[i]->len;
@@ -752,6 +764,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             ctx += n.node->ntok;
             if (!n.tensor) push_blocks(n.node->blocks, n.node->ntok);
         }
+        req_fold_blk[i] = (int32_t)(pl->req_blk.size() - fold0);
         if (!skip_suffix[i]) push_blocks(R[i]->blocks, R[i]->len);
         unshared += (double)ctx * hkv * D * 4;
     }
@@ -907,7 +920,10 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
                 const uint32_t e = pl->req_blk[rb + (x - b0)];
                 const uint32_t slab = (e & kBlkMask) * (uint32_t)hkv + (uint32_t)head;
                 pl->k2_ent[2 * (size_t)x] = slab | (e & ~kBlkMask) | (x == b0 ? 0x80000000u : 0u);
-                pl->k2_ent[2 * (size_t)x + 1] = (uint32_t)(req * hkv + head);
+                // bit 31: a block of a folded prefix node, read by every request under the node:
+                // K2 streams it with the default L2 policy instead of evict_first
+                pl->k2_ent[2 * (size_t)x + 1] = (uint32_t)(req * hkv + head) |
+                                                ((x - b0) < req_fold_blk[req] && k2_shared_normal() ? 0x80000000u : 0u);
             }
             int32_t *um = &pl->unit_meta[(size_t)uu * 8];
             um[0] = b0; um[1] = b1; um[2] = req; um[3] = head;

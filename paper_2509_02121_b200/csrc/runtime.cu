@@ -413,6 +413,19 @@ bool force_wide() {
     return f;
 }
 
+// Experiment hook (HALO_K2_AUTO_NARROW=1): let the planner pick the narrow shape whenever
+// whole units balance on it.  By default only for short units (< 8 blocks on average):
+// since the L2 evict_first policy on the suffix stream (session 4) the wide shape wins at
+// C1 (17 blocks per unit: K2 0.81 vs 0.77 of HBM), while 1-2-block units (16-token
+// suffixes) stay 20% faster on the narrow one (K2).
+bool auto_narrow() {
+    static const bool f = [] {
+        const char *e = getenv("HALO_K2_AUTO_NARROW");
+        return e && atoi(e) != 0;
+    }();
+    return f;
+}
+
 // Test hook (HALO_K2_FORCE_NARROW=1): always use K2's narrow launch shape.
 bool force_narrow() {
     static const bool f = [] {
@@ -861,7 +874,8 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             cuts = equal_cuts(Wn, kK2WarpsNarrow);
         } else if (force_wide()) {  // experiment hook
             cuts = equal_cuts(Ww, kK2WarpsWide);
-        } else if (U < 2 * Ww && (cuts = snapped_cuts(Wn, kK2WarpsNarrow, bal), bal)) {
+        } else if ((auto_narrow() || Btot < 8 * (int64_t)U) && U < 2 * Ww &&
+                   (cuts = snapped_cuts(Wn, kK2WarpsNarrow, bal), bal)) {
             // few units per warp (stream-K pieces would dominate) and whole units divide
             // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
             pl->k2_warps = kK2WarpsNarrow;

@@ -232,19 +232,74 @@ halo_status halo_plan_export(halo_plan plan, int32_t which, void *dst, int64_t c
 halo_status halo_plan_destroy(halo_plan plan);
 
 /* ------------------------------------------------------------------ migration */
-/* NCCL point-to-point over NVLink/NVSwitch, used ONLY for KV-block migration.  The 128-B
- * ncclUniqueId is created on one rank and broadcast by the caller (torch.distributed). */
+/* KV-block migration between GPUs: "cache snapshots can be migrated directly among GPUs via
+ * NVLink ... under scheduler control" (PAPER.md:337 §3.3; NVLink, :673 §4.5), overlapped
+ * with decode attention (PAPER.md:9 abstract, :59 §1).  NCCL point-to-point over
+ * NVLink/NVSwitch is used ONLY here.  The 128-B ncclUniqueId is created on one rank
+ * (halo_comm_unique_id) and broadcast by the caller (torch.distributed).
+ *
+ * Wire format (both peers derive it from the node's token count and the pool geometry, which
+ * must agree: num_layers, num_kv_heads, head_dim): the node's blocks flattened layer-major
+ * into items j = layer * nblk + b (nblk = ceil(ntok/16)); item j is the whole (layer, block)
+ * slab of K then of V, [hkv][16][d] bf16 each (partial last block: its zero tail moves too,
+ * so every destination slab is bit-identical to its source slab).  A transfer is cut into
+ * chunks of chunk_items = max(1, chunk_bytes / item_bytes) items; chunk c of every transfer
+ * of one exchange call moves in round c, each round ONE ncclGroupStart/End (so a pair of
+ * ranks that send to each other in the same call cannot deadlock), double-buffered: the K4
+ * pack of round c+1 and the K4 unpack of round c-1 (on `stream`) overlap the NCCL transfer of
+ * round c (on a library side stream). */
+typedef struct {
+    int32_t max_ctas;     /* NCCL maxCTAs of the communicator (bounds the SMs NCCL takes from
+                             decode while a migration runs); <= 0: NCCL's default          */
+    int32_t copy_ctas;    /* CTAs of the K4 pack / unpack kernels; <= 0: 8 x SM count       */
+    int64_t chunk_bytes;  /* bytes per transfer per round (K+V); <= 0: 32 MiB.  MUST be equal
+                             on every rank (it fixes the wire chunking).                    */
+} halo_comm_config;
+
 halo_status halo_comm_unique_id(void *id_out /* 128 bytes */);
+/* Create the pool's communicator (collective over the nranks ranks: every rank calls it with
+ * the same id).  nranks == 1 is a valid self-loop communicator (loopback migration on one
+ * GPU: the exact pack -> NCCL -> unpack -> register pipeline).  cfg nullable (defaults).
+ * EBUSY if the pool already has one; ENCCL if libnccl.so.2 is unavailable or NCCL fails. */
 halo_status halo_comm_init(halo_pool pool, const void *id /* 128 bytes */, int32_t nranks,
                            int32_t rank);
-/* Send node `node` (all layers, the pool's kv heads) to `dst_rank`: K4 pack into chunk
- * buffers pipelined with ncclSend on an internal side stream ordered after `stream`; on
- * return `stream` is ordered after the last send.  mode 0 = MOVE (node released after
- * the transfer; EBUSY if referenced), 1 = COPY.  Both peers must call concurrently. */
+halo_status halo_comm_init_config(halo_pool pool, const void *id /* 128 bytes */, int32_t nranks,
+                                  int32_t rank, const halo_comm_config *cfg);
+
+typedef struct {
+    int64_t node;     /* node to send (device-resident)                                       */
+    int32_t peer;     /* destination rank; may be this rank (self loop, matched by a recv of
+                         the same call)                                                       */
+    int32_t mode;     /* 0 = MOVE (node released once the transfer has passed; EBUSY if it has
+                         children or open requests), 1 = COPY                                  */
+} halo_migrate_send_op;
+
+typedef struct {
+    int64_t parent;   /* register the received node under this node (-1 = a root)           */
+    int32_t peer;     /* source rank; may be this rank                                         */
+    int32_t ntok;     /* tokens of the node being received (>= 1; the sender's ntok)           */
+} halo_migrate_recv_op;
+
+/* One batch of migrations on this rank: send sends[0..nsend) and receive recvs[0..nrecv)
+ * (HOST arrays; either count may be 0).  Every rank taking part calls it at the same point of
+ * its NCCL program.  Pairing: the k-th send of rank a to peer b matches the k-th recv of rank
+ * b from peer a (NCCL point-to-point order), with equal token counts -- the caller's
+ * scheduler guarantees this (relocation.rank_actions); for self-loop ops the library checks
+ * it (EINVAL).  Received nodes are registered in recv order; their ids go to nodes_out[nrecv]
+ * (HOST).  Validation (ids, peers, modes, MOVE of a referenced or twice-listed node, parents,
+ * and the allocation of every destination block: ENOMEM) completes before any device work;
+ * on error nothing changes.  Stream-ordered: pack and unpack kernels run on `stream` (pass a
+ * side stream to overlap decode on another one), NCCL on a library stream; on return `stream`
+ * is ordered after every send and receive of the call.  The received nodes may be used (plans,
+ * requests) immediately in `stream` order.  Sources of MOVEs are released (their blocks return
+ * to the pool once `stream` has passed this call). */
+halo_status halo_migrate_exchange(halo_pool pool, int32_t nsend, const halo_migrate_send_op *sends,
+                                  int32_t nrecv, const halo_migrate_recv_op *recvs, void *stream,
+                                  int64_t *nodes_out);
+/* One send (== halo_migrate_exchange with one send op).  dst_rank != this rank. */
 halo_status halo_migrate_send(halo_pool pool, int64_t node, int32_t dst_rank, int32_t mode,
                               void *stream);
-/* Receive a node of `ntok` tokens from `src_rank` into fresh blocks and register it under
- * `parent` (-1 = root).  ncclRecv pipelined with the K4 unpack kernel. */
+/* One receive (== halo_migrate_exchange with one recv op).  src_rank != this rank. */
 halo_status halo_migrate_recv(halo_pool pool, int32_t src_rank, int64_t parent, int32_t ntok,
                               void *stream, int64_t *node_out);
 /* Same-device relocation ("cache snapshots ... migrated"): copy `node` of

@@ -54,6 +54,18 @@ class PlaceMove(C.Structure):
     _fields_ = [("item", _i32), ("src", _i32), ("dst", _i32), ("mode", _i32), ("seconds", C.c_double)]
 
 
+class CommConfig(C.Structure):
+    _fields_ = [("max_ctas", _i32), ("copy_ctas", _i32), ("chunk_bytes", _i64)]
+
+
+class MigrateSendOp(C.Structure):
+    _fields_ = [("node", _i64), ("peer", _i32), ("mode", _i32)]
+
+
+class MigrateRecvOp(C.Structure):
+    _fields_ = [("parent", _i64), ("peer", _i32), ("ntok", _i32)]
+
+
 SIGNATURES = {
     "halo_last_error": (C.c_char_p, []),
     "halo_abi_version": (_i32, []),
@@ -83,6 +95,9 @@ SIGNATURES = {
     "halo_plan_destroy": (_i32, [_p]),
     "halo_comm_unique_id": (_i32, [_p]),
     "halo_comm_init": (_i32, [_p, _p, _i32, _i32]),
+    "halo_comm_init_config": (_i32, [_p, _p, _i32, _i32, C.POINTER(CommConfig)]),
+    "halo_migrate_exchange": (_i32, [_p, _i32, C.POINTER(MigrateSendOp), _i32, C.POINTER(MigrateRecvOp),
+                                     _p, _pi64]),
     "halo_migrate_send": (_i32, [_p, _i64, _i32, _i32, _p]),
     "halo_migrate_recv": (_i32, [_p, _i32, _i64, _i32, _p, _pi64]),
     "halo_prefix_clone": (_i32, [_p, _i64, _p, _i64, _p, _pi64]),
@@ -350,9 +365,23 @@ class Pool:
         return int(n.value)
 
     # ---- migration ----
-    def comm_init(self, uid: bytes, nranks: int, rank: int):
+    def comm_init(self, uid: bytes, nranks: int, rank: int, max_ctas: int = 0, copy_ctas: int = 0,
+                  chunk_bytes: int = 0):
         buf = C.create_string_buffer(uid, 128)
-        _call("halo_comm_init", self.handle, buf, nranks, rank)
+        if max_ctas or copy_ctas or chunk_bytes:
+            cfg = CommConfig(max_ctas, copy_ctas, chunk_bytes)
+            _call("halo_comm_init_config", self.handle, buf, nranks, rank, C.byref(cfg))
+        else:
+            _call("halo_comm_init", self.handle, buf, nranks, rank)
+
+    def migrate_exchange(self, sends=(), recvs=(), stream=None) -> list:
+        """sends: [(node, peer, mode)], recvs: [(peer, parent, ntok)] -> new node ids (recv order)."""
+        ns, nr = len(sends), len(recvs)
+        sa = (MigrateSendOp * max(ns, 1))(*[MigrateSendOp(n, pr, m) for n, pr, m in sends])
+        ra = (MigrateRecvOp * max(nr, 1))(*[MigrateRecvOp(par, pr, nt) for pr, par, nt in recvs])
+        out = (C.c_int64 * max(nr, 1))()
+        _call("halo_migrate_exchange", self.handle, ns, sa, nr, ra, self._s(stream), out)
+        return [int(out[i]) for i in range(nr)]
 
     def migrate_send(self, node: int, dst_rank: int, mode: int = 1, stream=None):
         _call("halo_migrate_send", self.handle, node, dst_rank, mode, self._s(stream))

@@ -110,4 +110,12 @@ cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const v
                                   const int32_t *pairs, int32_t nblk, int layer_begin,
                                   int layer_end, int num_sms, cudaStream_t s);
 
+// Migration K4 pack (to_pool = false) / unpack (true), block-granular: items
+// [item_begin, item_end) of the node's flattened [layer][block] list (layer = j / nblk,
+// pool block blocks[j % nblk]); wire layout [item][K|V][hkv][16][d] bf16.  At most max_ctas
+// CTAs of 256 threads (bounded so a migration can run beside decode).
+cudaError_t launch_kv_runs(const PoolGeom &g, void *pool_k, void *pool_v, void *buf,
+                           const int32_t *blocks, int32_t nblk, int64_t item_begin,
+                           int64_t item_end, bool to_pool, int max_ctas, cudaStream_t s);
+
 }  // namespace halo

@@ -161,6 +161,35 @@ __global__ void __launch_bounds__(256) kv_copy_blocks_kernel(
     }
 }
 
+// K4 pack / unpack for migration, block-granular: item j of [item_begin, item_end) is the
+// (layer j / nblk, node block blocks[j % nblk]) pair; its K run and its V run (hkv*16*d*2
+// bytes each, contiguous in the pool) go to / come from the wire buffer at
+// ((j - item_begin) * 2 + kv) * run16 int4.  A whole block moves, the zero tail of a partial
+// last block included, so the destination slab is bit-identical to the source slab.
+__global__ void __launch_bounds__(256) kv_runs_kernel(
+    int4 *__restrict__ pk, int4 *__restrict__ pv, int4 *__restrict__ buf,
+    const int32_t *__restrict__ blocks, int32_t nblk, int64_t item_begin, int64_t nitems2,
+    int32_t run16, int64_t pool_layer16, int to_pool) {
+    for (int64_t it = blockIdx.x; it < nitems2; it += gridDim.x) {
+        const int kv = (int)(it & 1);
+        const int64_t j = item_begin + (it >> 1);
+        const int64_t layer = j / nblk;
+        int4 *pool = (kv ? pv : pk) + layer * pool_layer16 + (int64_t)blocks[j % nblk] * run16;
+        int4 *wire = buf + it * run16;
+        const int4 *src = to_pool ? wire : pool;
+        int4 *dst = to_pool ? pool : wire;
+        for (int o0 = threadIdx.x; o0 < run16; o0 += 256 * kCopyUnroll) {
+            int4 v[kCopyUnroll];
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u)
+                if (o0 + u * 256 < run16) v[u] = ld_stream(src + o0 + u * 256);
+#pragma unroll
+            for (int u = 0; u < kCopyUnroll; ++u)
+                if (o0 + u * 256 < run16) dst[o0 + u * 256] = v[u];
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const void *src_v,
@@ -211,6 +240,20 @@ cudaError_t launch_kv_gather(const PoolGeom &pg, const void *pool_k, const void 
     kv_gather_kernel<<<grid, threads, 0, s>>>((const int4 *)pool_k, (const int4 *)pool_v,
                                               (int4 *)dst_k, (int4 *)dst_v, g, slots,
                                               layer_begin);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kv_runs(const PoolGeom &pg, void *pool_k, void *pool_v, void *buf,
+                           const int32_t *blocks, int32_t nblk, int64_t item_begin,
+                           int64_t item_end, bool to_pool, int max_ctas, cudaStream_t s) {
+    const int64_t nitems2 = 2 * (item_end - item_begin);
+    if (nblk == 0 || nitems2 <= 0) return cudaSuccess;
+    const int32_t run16 = pg.hkv * kBlockTok * pg.d * 2 / 16;
+    int64_t grid = nitems2;
+    if (grid > max_ctas) grid = max_ctas;
+    kv_runs_kernel<<<(unsigned)grid, 256, 0, s>>>((int4 *)pool_k, (int4 *)pool_v, (int4 *)buf, blocks,
+                                                  nblk, item_begin, nitems2, run16, pg.cap * run16,
+                                                  to_pool ? 1 : 0);
     return cudaGetLastError();
 }
 

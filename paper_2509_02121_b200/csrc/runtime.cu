@@ -109,6 +109,9 @@ struct NcclApi {
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *) = nullptr;
 };
 
 const NcclApi &nccl() {
@@ -123,7 +126,11 @@ const NcclApi &nccl() {
         a.Send = (decltype(a.Send))dlsym(h, "ncclSend");
         a.Recv = (decltype(a.Recv))dlsym(h, "ncclRecv");
         a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
-        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GetErrorString;
+        a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+        a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+        a.CommInitRankConfig = (decltype(a.CommInitRankConfig))dlsym(h, "ncclCommInitRankConfig");
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GetErrorString &&
+               a.GroupStart && a.GroupEnd;
         return a;
     }();
     return api;
@@ -1129,23 +1136,21 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
     return HALO_OK;
 }
 
-// Chunk of layers per migration message: ~32 MiB of K+V.
-int layers_per_chunk(halo_pool p, int32_t ntok) {
-    const size_t per_layer = (size_t)ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2 * 2;
-    size_t l = ((size_t)32 << 20) / std::max<size_t>(per_layer, 1);
-    if (l < 1) l = 1;
-    if (l > (size_t)p->cfg.num_layers) l = p->cfg.num_layers;
-    return (int)l;
-}
-
+// Migration staging buffer (both parities of every transfer's send or receive slice).  A
+// grow waits for the previous exchange's last use of the old buffer (mig_done on its stream).
 halo_status ensure_mig(halo_pool p, size_t bytes) {
     if (p->mig_cap >= bytes) return HALO_OK;
     if (p->mig_buf) {
-        HALO_CUDA(cudaDeviceSynchronize());
-        cudaFree(p->mig_buf);
+        if (p->mig_done) HALO_CUDA(cudaEventSynchronize(p->mig_done));
+        HALO_CUDA(cudaFree(p->mig_buf));
         p->mig_buf = nullptr;
+        p->mig_cap = 0;
     }
-    HALO_CUDA(cudaMalloc(&p->mig_buf, bytes));
+    if (cudaMalloc(&p->mig_buf, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        p->mig_buf = nullptr;
+        return fail(HALO_ENOMEM, "migration staging buffer of %zu bytes", bytes);
+    }
     p->mig_cap = bytes;
     return HALO_OK;
 }
@@ -1355,6 +1360,7 @@ halo_status halo_pool_destroy(halo_pool p) {
         for (cudaEvent_t e : p->event_cache) cudaEventDestroy(e);
         for (cudaEvent_t e : p->mig_ev)
             if (e) cudaEventDestroy(e);
+        if (p->mig_done) cudaEventDestroy(p->mig_done);
         if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
         if (p->side) cudaStreamDestroy(p->side);
         if (p->mig_buf) cudaFree(p->mig_buf);
@@ -2041,130 +2047,243 @@ halo_status halo_comm_unique_id(void *id_out) {
     return HALO_OK;
 }
 
-halo_status halo_comm_init(halo_pool p, const void *id, int32_t nranks, int32_t rank) {
+halo_status halo_comm_init_config(halo_pool p, const void *id, int32_t nranks, int32_t rank,
+                                  const halo_comm_config *cfg) {
     HALO_GUARD_BEGIN
     if (check_pool(p)) return HALO_EINVAL;
     if (p->host_only) return fail(HALO_EUNSUPPORTED, "host-only pool");
     if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(HALO_EINVAL, "bad communicator arguments");
     if (p->comm) return fail(HALO_EBUSY, "communicator already initialised");
+    halo_comm_config c{};
+    if (cfg) c = *cfg;
+    if (c.chunk_bytes <= 0) c.chunk_bytes = (int64_t)32 << 20;
+    if (c.copy_ctas <= 0) c.copy_ctas = 8 * p->num_sms;
     DeviceGuard dg(p);
     ncclUniqueId uid;
     memcpy(&uid, id, sizeof uid);
-    HALO_NCCL(nccl().CommInitRank(&p->comm, nranks, uid, rank));
+    if (c.max_ctas > 0) {
+        if (!nccl().CommInitRankConfig) return fail(HALO_ENCCL, "ncclCommInitRankConfig unavailable");
+        ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+        nc.maxCTAs = c.max_ctas;
+        nc.minCTAs = 1;
+        HALO_NCCL(nccl().CommInitRankConfig(&p->comm, nranks, uid, rank, &nc));
+    } else {
+        HALO_NCCL(nccl().CommInitRank(&p->comm, nranks, uid, rank));
+    }
     p->nranks = nranks;
     p->rank = rank;
+    p->mig_cfg = c;
     if (!p->side) HALO_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     for (auto &e : p->mig_ev)
         if (!e) HALO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!p->mig_done) HALO_CUDA(cudaEventCreateWithFlags(&p->mig_done, cudaEventDisableTiming));
+    return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_comm_init(halo_pool p, const void *id, int32_t nranks, int32_t rank) {
+    return halo_comm_init_config(p, id, nranks, rank, nullptr);
+}
+
+namespace {
+
+// One transfer of an exchange: a send (pack + ncclSend) or a receive (ncclRecv + unpack).
+struct Xfer {
+    bool send;
+    int32_t peer;
+    int64_t nblk, items, nchunks;
+    const std::vector<int32_t> *blocks;  // pool blocks in token order (source or destination)
+    int64_t dev_off;                     // offset of the block list in the uploaded array
+    size_t slice;                        // buffer bytes per parity
+    size_t buf_off;                      // offset of the parity-0 slice
+};
+
+}  // namespace
+
+halo_status halo_migrate_exchange(halo_pool p, int32_t nsend, const halo_migrate_send_op *sends, int32_t nrecv,
+                                  const halo_migrate_recv_op *recvs, void *stream, int64_t *nodes_out) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (!p->comm) return fail(HALO_ENCCL, "no communicator (halo_comm_init)");
+    if (nsend < 0 || nrecv < 0 || (nsend && !sends) || (nrecv && (!recvs || !nodes_out)))
+        return fail(HALO_EINVAL, "bad op arrays");
+    if (nsend + nrecv == 0) return HALO_OK;
+    // ---- validation (nothing changes on error)
+    std::vector<int64_t> moved;
+    std::vector<int32_t> self_send_tok, self_recv_tok;
+    for (int32_t i = 0; i < nsend; ++i) {
+        const auto &o = sends[i];
+        auto it = p->nodes.find(o.node);
+        if (it == p->nodes.end()) return fail(HALO_ENOENT, "send %d: unknown node %lld", i, (long long)o.node);
+        if (it->second.on_host) return fail(HALO_EBUSY, "send %d: node %lld is offloaded: fetch it first", i, (long long)o.node);
+        if (o.peer < 0 || o.peer >= p->nranks) return fail(HALO_EINVAL, "send %d: bad peer %d", i, o.peer);
+        if (o.mode != 0 && o.mode != 1) return fail(HALO_EINVAL, "send %d: mode must be 0 (MOVE) or 1 (COPY)", i);
+        if (o.mode == 0) {
+            if (it->second.children || it->second.requests)
+                return fail(HALO_EBUSY, "send %d: MOVE of node %lld with %d children and %d requests", i,
+                            (long long)o.node, it->second.children, it->second.requests);
+            if (std::find(moved.begin(), moved.end(), o.node) != moved.end())
+                return fail(HALO_EINVAL, "send %d: node %lld moved twice", i, (long long)o.node);
+            moved.push_back(o.node);
+        }
+        if (o.peer == p->rank) self_send_tok.push_back(it->second.ntok);
+    }
+    for (int32_t i = 0; i < nrecv; ++i) {
+        const auto &o = recvs[i];
+        if (o.ntok < 1) return fail(HALO_EINVAL, "recv %d: ntok must be >= 1", i);
+        if (o.peer < 0 || o.peer >= p->nranks) return fail(HALO_EINVAL, "recv %d: bad peer %d", i, o.peer);
+        if (o.parent < -1) return fail(HALO_EINVAL, "recv %d: bad parent id", i);
+        if (o.parent >= 0) {
+            auto pit = p->nodes.find(o.parent);
+            if (pit == p->nodes.end()) return fail(HALO_ENOENT, "recv %d: unknown parent %lld", i, (long long)o.parent);
+            if (pit->second.on_host) return fail(HALO_EBUSY, "recv %d: parent %lld is offloaded", i, (long long)o.parent);
+            if (std::find(moved.begin(), moved.end(), o.parent) != moved.end())
+                return fail(HALO_EINVAL, "recv %d: parent %lld is moved away by this call", i, (long long)o.parent);
+        }
+        if (o.peer == p->rank) self_recv_tok.push_back(o.ntok);
+    }
+    if (self_send_tok != self_recv_tok)
+        return fail(HALO_EINVAL, "self-loop sends and receives do not pair up (count or token counts differ)");
+    DeviceGuard dg(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t run_bytes = (int64_t)p->cfg.num_kv_heads * kBlockTok * p->cfg.head_dim * 2;
+    const int64_t item_bytes = 2 * run_bytes;  // K and V slab of one (layer, block)
+    const int64_t R = std::max<int64_t>(1, p->mig_cfg.chunk_bytes / item_bytes);
+    const int L = p->cfg.num_layers;
+    // ---- destination blocks (all or nothing)
+    std::vector<std::vector<int32_t>> dst(nrecv);
+    for (int32_t i = 0; i < nrecv; ++i) {
+        halo_status st = alloc_blocks(p, ceil_div(recvs[i].ntok, kBlockTok), dst[i]);
+        if (st != HALO_OK) {
+            for (int32_t j = i; j >= 0; --j) unalloc_blocks(p, dst[j], 0);
+            return st;
+        }
+    }
+    auto undo = [&]() {
+        for (int32_t j = nrecv - 1; j >= 0; --j) unalloc_blocks(p, dst[j], 0);
+    };
+    // ---- transfers, buffer slices, block lists
+    std::vector<Xfer> xs;
+    std::vector<int32_t> lists;
+    size_t per_parity = 0;
+    int64_t rounds = 0;
+    auto add = [&](bool snd, int32_t peer, const std::vector<int32_t> *blocks) {
+        Xfer x;
+        x.send = snd;
+        x.peer = peer;
+        x.nblk = (int64_t)blocks->size();
+        x.items = x.nblk * L;
+        x.nchunks = ceil_div(x.items, R);
+        x.blocks = blocks;
+        x.dev_off = (int64_t)lists.size();
+        lists.insert(lists.end(), blocks->begin(), blocks->end());
+        x.slice = (size_t)(std::min(R, x.items) * item_bytes);
+        x.buf_off = per_parity;
+        per_parity += x.slice;
+        rounds = std::max(rounds, x.nchunks);
+        xs.push_back(x);
+    };
+    for (int32_t i = 0; i < nsend; ++i) add(true, sends[i].peer, &p->nodes[sends[i].node].blocks);
+    for (int32_t i = 0; i < nrecv; ++i) add(false, recvs[i].peer, &dst[i]);
+    halo_status st = ensure_mig(p, 2 * per_parity);
+    Scratch sl;
+    if (st == HALO_OK) st = upload(lists.data(), lists.size() * 4, s, sl);
+    if (st != HALO_OK) {
+        undo();
+        return st;
+    }
+    // ---- rounds: pack(c) on s | one NCCL group of every transfer's chunk c on side | unpack(c-1)
+    // on s.  Buffer reuse is ordered by construction: pack(c) follows unpack(c-2) on s, which
+    // waited for round c-2; round c waits for pack(c).
+    uint8_t *base = static_cast<uint8_t *>(p->mig_buf);
+    cudaEvent_t *ev_packed = p->mig_ev, *ev_xfer = p->mig_ev + 2;
+    const int32_t *dlist = static_cast<const int32_t *>(sl.ptr);
+    const int ctas = p->mig_cfg.copy_ctas;
+    auto unpack = [&](int64_t c) -> halo_status {
+        const int b = (int)(c & 1);
+        HALO_CUDA(cudaStreamWaitEvent(s, ev_xfer[b], 0));
+        for (auto &x : xs) {
+            if (x.send || c >= x.nchunks) continue;
+            const int64_t i0 = c * R, i1 = std::min(x.items, i0 + R);
+            cudaError_t e = launch_kv_runs(p->geom, p->k, p->v, base + b * per_parity + x.buf_off,
+                                           dlist + x.dev_off, (int32_t)x.nblk, i0, i1, true, ctas, s);
+            if (e != cudaSuccess) return fail(HALO_ECUDA, "unpack launch: %s", cudaGetErrorString(e));
+        }
+        return HALO_OK;
+    };
+    // From the first launch on, an error leaves the exchange half-enqueued: the communicator
+    // is unusable (peers wait), so it is reported as is.
+    for (int64_t c = 0; c < rounds; ++c) {
+        const int b = (int)(c & 1);
+        for (auto &x : xs) {
+            if (!x.send || c >= x.nchunks) continue;
+            const int64_t i0 = c * R, i1 = std::min(x.items, i0 + R);
+            cudaError_t e = launch_kv_runs(p->geom, p->k, p->v, base + b * per_parity + x.buf_off,
+                                           dlist + x.dev_off, (int32_t)x.nblk, i0, i1, false, ctas, s);
+            if (e != cudaSuccess) return fail(HALO_ECUDA, "pack launch: %s", cudaGetErrorString(e));
+        }
+        HALO_CUDA(cudaEventRecord(ev_packed[b], s));
+        HALO_CUDA(cudaStreamWaitEvent(p->side, ev_packed[b], 0));
+        HALO_NCCL(nccl().GroupStart());
+        for (auto &x : xs) {
+            if (c >= x.nchunks) continue;
+            const int64_t i0 = c * R, i1 = std::min(x.items, i0 + R);
+            void *buf = base + b * per_parity + x.buf_off;
+            const size_t bytes = (size_t)((i1 - i0) * item_bytes);
+            ncclResult_t r = x.send ? nccl().Send(buf, bytes, ncclUint8, x.peer, p->comm, p->side)
+                                    : nccl().Recv(buf, bytes, ncclUint8, x.peer, p->comm, p->side);
+            if (r != ncclSuccess) {
+                nccl().GroupEnd();
+                return fail(HALO_ENCCL, "nccl %s of round %lld: %s", x.send ? "send" : "recv", (long long)c,
+                            nccl().GetErrorString(r));
+            }
+        }
+        HALO_NCCL(nccl().GroupEnd());
+        HALO_CUDA(cudaEventRecord(ev_xfer[b], p->side));
+        if (c > 0 && (st = unpack(c - 1)) != HALO_OK) return st;
+    }
+    if ((st = unpack(rounds - 1)) != HALO_OK) return st;  // also orders s after the last send
+    HALO_CUDA(cudaEventRecord(p->mig_done, s));
+    note_stream(p, s);
+    // ---- bookkeeping: MOVE sources released (reusable once s has passed), receives registered
+    for (int32_t i = 0; i < nsend; ++i) {
+        if (sends[i].mode != 0) continue;
+        auto it = p->nodes.find(sends[i].node);
+        if (it == p->nodes.end()) continue;  // (listed twice as COPY and MOVE: already gone)
+        const int64_t parent = it->second.parent;
+        release_blocks(p, std::move(it->second.blocks));
+        p->nodes.erase(it);
+        if (parent >= 0) p->nodes[parent].children--;
+        p->layout_gen++;
+    }
+    for (int32_t i = 0; i < nrecv; ++i) {
+        const int64_t id = p->next_id++;
+        Node n;
+        n.parent = recvs[i].parent;
+        n.ntok = recvs[i].ntok;
+        n.blocks = std::move(dst[i]);
+        p->nodes.emplace(id, std::move(n));
+        if (recvs[i].parent >= 0) p->nodes[recvs[i].parent].children++;
+        nodes_out[i] = id;
+    }
     return HALO_OK;
     HALO_GUARD_END
 }
 
 halo_status halo_migrate_send(halo_pool p, int64_t node, int32_t dst_rank, int32_t mode, void *stream) {
-    HALO_GUARD_BEGIN
     if (check_pool(p)) return HALO_EINVAL;
-    if (!p->comm) return fail(HALO_ENCCL, "no communicator (halo_comm_init)");
-    auto it = p->nodes.find(node);
-    if (it == p->nodes.end()) return fail(HALO_ENOENT, "unknown node %lld", (long long)node);
-    if (it->second.on_host) return fail(HALO_EBUSY, "node %lld is offloaded: fetch it first", (long long)node);
-    if (dst_rank < 0 || dst_rank >= p->nranks || dst_rank == p->rank) return fail(HALO_EINVAL, "bad destination rank");
-    if (mode != 0 && mode != 1) return fail(HALO_EINVAL, "mode must be 0 (MOVE) or 1 (COPY)");
-    if (mode == 0 && (it->second.children || it->second.requests))
-        return fail(HALO_EBUSY, "MOVE of a referenced node");
-    DeviceGuard dg(p);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int32_t ntok = it->second.ntok;
-    const int L = p->cfg.num_layers, lpc = layers_per_chunk(p, ntok);
-    const size_t layer_bytes = (size_t)ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
-    const size_t chunk_bytes = 2 * lpc * layer_bytes;  // K then V
-    halo_status st = ensure_mig(p, 2 * chunk_bytes);
-    if (st != HALO_OK) return st;
-    std::vector<int32_t> slots = token_slots(it->second.blocks, ntok);
-    Scratch ss;
-    if ((st = upload(slots.data(), slots.size() * 4, s, ss)) != HALO_OK) return st;
-    cudaEvent_t *ev_packed = p->mig_ev, *ev_sent = p->mig_ev + 2;
-    int c = 0;
-    for (int l0 = 0; l0 < L; l0 += lpc, ++c) {
-        const int l1 = std::min(L, l0 + lpc), b = c & 1;
-        uint8_t *buf = static_cast<uint8_t *>(p->mig_buf) + b * chunk_bytes;
-        const size_t half = (size_t)(l1 - l0) * layer_bytes;
-        if (c >= 2) HALO_CUDA(cudaStreamWaitEvent(s, ev_sent[b], 0));
-        cudaError_t e = launch_kv_gather(p->geom, p->k, p->v, buf, buf + half, (const int32_t *)ss.ptr, ntok, l0,
-                                         l1, p->num_sms, s);
-        if (e != cudaSuccess) return fail(HALO_ECUDA, "pack launch: %s", cudaGetErrorString(e));
-        HALO_CUDA(cudaEventRecord(ev_packed[b], s));
-        HALO_CUDA(cudaStreamWaitEvent(p->side, ev_packed[b], 0));
-        HALO_NCCL(nccl().Send(buf, 2 * half, ncclUint8, dst_rank, p->comm, p->side));
-        HALO_CUDA(cudaEventRecord(ev_sent[b], p->side));
-    }
-    HALO_CUDA(cudaStreamWaitEvent(s, ev_sent[(c - 1) & 1], 0));
-    if (c >= 2) HALO_CUDA(cudaStreamWaitEvent(s, ev_sent[c & 1], 0));
-    note_stream(p, s);
-    if (mode == 0) {
-        const int64_t parent = it->second.parent;
-        release_blocks(p, std::move(it->second.blocks));
-        p->nodes.erase(it);
-        if (parent >= 0) p->nodes[parent].children--;
-    }
-    return HALO_OK;
-    HALO_GUARD_END
+    if (dst_rank == p->rank) return fail(HALO_EINVAL, "send to self: use halo_migrate_exchange with the matching recv");
+    halo_migrate_send_op o{node, dst_rank, mode};
+    return halo_migrate_exchange(p, 1, &o, 0, nullptr, stream, nullptr);
 }
 
 halo_status halo_migrate_recv(halo_pool p, int32_t src_rank, int64_t parent, int32_t ntok, void *stream,
                               int64_t *node_out) {
-    HALO_GUARD_BEGIN
     if (check_pool(p)) return HALO_EINVAL;
-    if (!p->comm) return fail(HALO_ENCCL, "no communicator (halo_comm_init)");
-    if (!node_out || ntok < 1) return fail(HALO_EINVAL, "bad arguments");
-    if (src_rank < 0 || src_rank >= p->nranks || src_rank == p->rank) return fail(HALO_EINVAL, "bad source rank");
-    if (parent >= 0 && !p->nodes.count(parent)) return fail(HALO_ENOENT, "unknown parent %lld", (long long)parent);
-    DeviceGuard dg(p);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int64_t nblk = ceil_div(ntok, kBlockTok);
-    std::vector<int32_t> blocks;
-    halo_status st = alloc_blocks(p, nblk, blocks);
-    if (st != HALO_OK) return st;
-    const int L = p->cfg.num_layers, lpc = layers_per_chunk(p, ntok);
-    const size_t layer_bytes = (size_t)ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
-    const size_t chunk_bytes = 2 * lpc * layer_bytes;
-    if ((st = ensure_mig(p, 2 * chunk_bytes)) != HALO_OK) {
-        unalloc_blocks(p, blocks, 0);
-        return st;
-    }
-    std::vector<int32_t> slots = token_slots(blocks, nblk * kBlockTok);
-    Scratch ss;
-    if ((st = upload(slots.data(), slots.size() * 4, s, ss)) != HALO_OK) {
-        unalloc_blocks(p, blocks, 0);
-        return st;
-    }
-    cudaEvent_t *ev_recv = p->mig_ev, *ev_unpacked = p->mig_ev + 2;
-    HALO_CUDA(cudaEventRecord(ev_unpacked[0], s));
-    HALO_CUDA(cudaStreamWaitEvent(p->side, ev_unpacked[0], 0));
-    int c = 0;
-    for (int l0 = 0; l0 < L; l0 += lpc, ++c) {
-        const int l1 = std::min(L, l0 + lpc), b = c & 1;
-        uint8_t *buf = static_cast<uint8_t *>(p->mig_buf) + b * chunk_bytes;
-        const size_t half = (size_t)(l1 - l0) * layer_bytes;
-        if (c >= 2) HALO_CUDA(cudaStreamWaitEvent(p->side, ev_unpacked[b], 0));
-        HALO_NCCL(nccl().Recv(buf, 2 * half, ncclUint8, src_rank, p->comm, p->side));
-        HALO_CUDA(cudaEventRecord(ev_recv[b], p->side));
-        HALO_CUDA(cudaStreamWaitEvent(s, ev_recv[b], 0));
-        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, buf, buf + half, ntok, (const int32_t *)ss.ptr, ntok,
-                                          nblk * kBlockTok - ntok, l0, l1, p->num_sms, s);
-        if (e != cudaSuccess) return fail(HALO_ECUDA, "unpack launch: %s", cudaGetErrorString(e));
-        HALO_CUDA(cudaEventRecord(ev_unpacked[b], s));
-    }
-    note_stream(p, s);
-    const int64_t id = p->next_id++;
-    Node n;
-    n.parent = parent;
-    n.ntok = ntok;
-    n.blocks = std::move(blocks);
-    p->nodes.emplace(id, std::move(n));
-    if (parent >= 0) p->nodes[parent].children++;
-    *node_out = id;
-    return HALO_OK;
-    HALO_GUARD_END
+    if (src_rank == p->rank) return fail(HALO_EINVAL, "recv from self: use halo_migrate_exchange with the matching send");
+    if (!node_out) return fail(HALO_EINVAL, "null node_out");
+    halo_migrate_recv_op o{parent, src_rank, ntok};
+    return halo_migrate_exchange(p, 0, nullptr, 1, &o, stream, node_out);
 }
 
 halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_t parent_dst, void *stream,

@@ -128,7 +128,9 @@ struct halo_pool_s {
     cudaStream_t side = nullptr;
     void *mig_buf = nullptr;
     size_t mig_cap = 0;
-    cudaEvent_t mig_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t mig_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // packed[2], transferred[2]
+    cudaEvent_t mig_done = nullptr;  // last use of mig_buf (end of the last exchange)
+    halo_comm_config mig_cfg{};
 };
 
 struct halo_plan_s {

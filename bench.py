@@ -377,6 +377,19 @@ def main():
                     help="gloo: debug the N>1 path with several ranks on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (rank 0 prints the line)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+               str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if int(os.environ.get("WORLD_SIZE", 1)) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', 1)}")
     if args.impl == "reference":
         return run_reference(args)
 
@@ -459,7 +472,8 @@ def main():
             torch.cuda.synchronize()
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
-        guarded("migration", lambda: measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist))
+        guarded("migration", lambda: measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist,
+                                                       decode_step=step))
     # ---- host paging of the template node (NEXT-2) ----
     if not args.no_migration and not args.profile:
         guarded("paging", lambda: measure_paging(pool, ld, wl, torch))
@@ -683,7 +697,10 @@ def measure_relocation(halo, mig):
     from paper_2509_02121_b200.relocation import plan_relocation
     from synth import make_config
     hbm, tc = peaks()[:2]
-    link = mig.get("GB/s", 0.0) * 1e9 if "nvlink_roofline" in mig else 900e9
+    link, link_src = NVLINK_PEER_GBS * 1e9, "measured NVLink peer copy per direction (B200_PROFILING.md)"
+    for e in mig.get("sweep", []):  # N>1: this run's measured rank0 -> rank1 rate, largest node
+        if e.get("pairs_0_to_k"):
+            link, link_src = e["pairs_0_to_k"][0]["GB/s"] * 1e9, "this run: NCCL rank0 -> rank1"
     wl = make_config("analytics", templates=64)
     out = {}
     for w in (1, 8, 64):
@@ -699,125 +716,246 @@ def measure_relocation(halo, mig):
     total = sum(it["exec_s"] for it in items)
     out.update({"what": "C3 batch (64 templates, all KV on worker 0) placed over 8 workers, "
                         "256 decode steps; planner = native beam search (host)",
-                "link_GBps": link / 1e9, "all_on_one_worker_s": total,
+                "link_GBps": link / 1e9, "link_source": link_src, "all_on_one_worker_s": total,
                 "lower_bound_s": total / 8})
     return out
 
 
-def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist):
-    """K4 / relocation copies of the C1 template node (2048 tokens x 32 layers x 8 heads =
-    256 MiB of K+V).  Every copy is timed with CUDA events on the launching stream after two
-    warm-up calls; HBM roofline = (read + write bytes) / time vs the measured copy peak.
-    N=1: pack (K4 gather to the exchange layout, halo_prefix_read), unpack (registration
-    from a device exchange buffer, halo_prefix_register), and same-GPU relocation
-    (halo_prefix_clone: pool-to-pool whole-block copy).  N>1: NCCL send/recv rank0 -> rank1."""
-    node = ld.node_ids[0]
-    ntok = wl.nodes[0].ntok
-    nbytes = ntok * wl.layers * wl.hkv * wl.d * 2 * 2
+def _timed(fn, stream, torch, reps=3, warm=2):
+    """Best of `reps` CUDA-event timings of fn() on `stream` after `warm` warm-up calls."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return best
+
+
+def _node_bytes(wl, ntok):
+    return ntok * wl.layers * wl.hkv * wl.d * 2 * 2
+
+
+def measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist, decode_step=None):
+    """KV-block migration (PAPER.md:337 §3.3, :673 §4.5) of prefix nodes of 1k..32k tokens x
+    32 layers x 8 kv heads (128 MiB..4 GiB of K+V: BASELINE configs[4], C4) through
+    halo_migrate_exchange: K4 block pack -> ncclSend/ncclRecv (one group per 32-MiB chunk
+    round) -> K4 unpack -> registration, timed with CUDA events on the migration stream.
+    N=1: a 1-rank NCCL communicator (self send/recv): the whole pipeline on one GPU, NVLink
+    not exercised; every byte moved costs 6 bytes of HBM traffic (pack r+w, NCCL r+w, unpack
+    r+w), so it is reported against the HBM roofline, labelled "loopback".  N>1: rank 0 -> k
+    pairs and the all-rank ring permutation, against the measured NVLink peer rate.  Both:
+    the migration on a side stream concurrent with C1 decode steps on the compute stream
+    (decode slowdown and migration GB/s under decode; PAPER.md:9, :59 overlap)."""
     hbm_peak = peaks()[0]
     stream = torch.cuda.current_stream()
+    sizes = (1024, 2048, 4096, 8192, 16384, 32768)
+    maxblk = (max(sizes) + 15) // 16
+    mp = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, 2 * maxblk + 64, dev)
+    uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
+    if world > 1:
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    mp.comm_init(uid, world, rank)
+    res = {"chunk_bytes": 32 << 20}
 
-    def timed(fn, reps=3):
-        for _ in range(2):
-            fn()
+    def make_node(ntok, seed):
+        kx = torch.empty((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
+        g = torch.Generator(device=f"cuda:{dev}").manual_seed(seed)
+        kx.normal_(generator=g)
+        vx = torch.empty_like(kx).normal_(generator=g)
+        n = mp.register_prefix(-1, ntok, kx, vx, stream)
         torch.cuda.synchronize()
-        best = None
-        for _ in range(reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            fn()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
-            best = ms if best is None else min(best, ms)
-        return best
-
-    def entry(ms, what):
-        return {"what": what, "bytes": nbytes, "ms": ms, "GB/s": nbytes / ms / 1e6,
-                "hbm_roofline": {"bound": "hbm", "achieved": 2 * nbytes / ms / 1e6, "peak": hbm_peak,
-                                 "unit": "GB/s", "frac": 2 * nbytes / ms / 1e6 / hbm_peak}}
+        return n
 
     if world == 1:
-        res = {"mode": "N=1: no NCCL; K4 pack, K4 unpack and same-GPU relocation timed separately"}
+        res["mode"] = ("loopback: 1-rank NCCL communicator on one GPU (self send/recv); pack -> NCCL "
+                       "-> unpack -> register, the exact multi-GPU pipeline, NVLink not exercised")
+        sweep = []
+        for ntok in sizes:
+            nd = make_node(ntok, ntok)
+            nb = _node_bytes(wl, ntok)
+
+            def loop():
+                (n2,) = mp.migrate_exchange(sends=[(nd, 0, 1)], recvs=[(0, -1, ntok)], stream=stream)
+                mp.release_prefix(n2)
+            ms = _timed(loop, stream, torch)
+            sweep.append({"tokens": ntok, "bytes": nb, "ms": ms, "loopback_GB/s": nb / ms / 1e6,
+                          "hbm_roofline": {"bound": "hbm", "achieved": 6 * nb / ms / 1e6, "peak": hbm_peak,
+                                           "unit": "GB/s", "frac": 6 * nb / ms / 1e6 / hbm_peak,
+                                           "traffic_model": "6 bytes of HBM per byte moved"}})
+            mp.release_prefix(nd)
+        res["loopback_sweep"] = sweep
+        # the K4 block pack alone (one chunk-free call: pool -> exchange layout of the C1 node)
+        node, ntok = ld.node_ids[0], wl.nodes[0].ntok
         kx = torch.empty((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
         vx = torch.empty_like(kx)
-        ms = timed(lambda: pool.read_prefix(node, kx, vx, stream))
-        res["pack"] = entry(ms, "K4 gather: pool blocks -> exchange layout [layer][token][head][d]")
-        dst = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, (ntok + 15) // 16 * 4, dev)
-
-        def unpack():
-            n = dst.register_prefix(-1, ntok, kx, vx, stream)
-            dst.release_prefix(n)
-        ms = timed(unpack)
-        res["unpack"] = entry(ms, "K4 scatter: exchange layout -> fresh pool blocks (register)")
-
-        def clone():
-            n = pool.clone_prefix(node, dst, -1, stream)
-            dst.release_prefix(n)
-        ms = timed(clone)
-        res["relocate"] = entry(ms, "same-GPU relocation: pool-to-pool whole-block copy")
-        torch.cuda.synchronize()
-        dst.destroy()
+        nb = _node_bytes(wl, ntok)
+        ms = _timed(lambda: pool.read_prefix(node, kx, vx, stream), stream, torch)
+        res["pack_c1_template"] = {"what": "K4 gather of the C1 template (halo_prefix_read)", "bytes": nb,
+                                   "ms": ms, "hbm_frac": 2 * nb / ms / 1e6 / hbm_peak}
         del kx, vx
-        # C4 shape on one GPU: nodes of 1k..32k tokens x 32 layers x 8 heads (128 MiB..4 GiB
-        # of K+V), K4 pack and same-GPU relocation GB/s vs node size
-        sweep = []
-        big = (32768 + 15) // 16
-        src = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, big + 16, dev)
-        dst = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, big + 16, dev)
-        for ntok in (1024, 2048, 4096, 8192, 16384, 32768):
-            kx = torch.empty((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
-            vx = torch.empty_like(kx)
-            kx.normal_()
-            vx.normal_()
-            nd = src.register_prefix(-1, ntok, kx, vx, stream)
-            nb = ntok * wl.layers * wl.hkv * wl.d * 2 * 2
+    else:
+        res["mode"] = f"NCCL over NVLink/NVSwitch, {world} ranks"
+        pairs = []
+        for ntok in (2048, 32768):
+            nd = make_node(ntok, ntok + rank)
+            nb = _node_bytes(wl, ntok)
+            per_k = []
+            for k in range(1, world):
+                def pair():
+                    if rank == 0:
+                        mp.migrate_exchange(sends=[(nd, k, 1)], stream=stream)
+                    elif rank == k:
+                        (n2,) = mp.migrate_exchange(recvs=[(0, -1, ntok)], stream=stream)
+                        mp.release_prefix(n2)
+                ms = _ranked_timed(pair, stream, torch, dist, dev)
+                per_k.append({"dst": k, "ms": ms, "GB/s": nb / ms / 1e6,
+                              "nvlink_frac": nb / ms / 1e6 / NVLINK_PEER_GBS})
+            pairs.append({"tokens": ntok, "bytes": nb, "pairs_0_to_k": per_k})
 
-            def clone2():
-                n2 = src.clone_prefix(nd, dst, -1, stream)
-                dst.release_prefix(n2)
-            ms_c = timed(clone2)
-            ms_p = timed(lambda: src.read_prefix(nd, kx, vx, stream))
-            sweep.append({"tokens": ntok, "bytes": nb, "relocate_ms": ms_c,
-                          "relocate_hbm_frac": 2 * nb / ms_c / 1e6 / hbm_peak,
-                          "pack_ms": ms_p, "pack_hbm_frac": 2 * nb / ms_p / 1e6 / hbm_peak})
-            torch.cuda.synchronize()
-            src.release_prefix(nd)
-            del kx, vx
+            def ring():
+                (n2,) = mp.migrate_exchange(sends=[(nd, (rank + 1) % world, 1)],
+                                            recvs=[((rank - 1) % world, -1, ntok)], stream=stream)
+                mp.release_prefix(n2)
+            ms = _ranked_timed(ring, stream, torch, dist, dev)
+            pairs[-1]["ring_permutation"] = {"ms": ms, "per_gpu_send_GB/s": nb / ms / 1e6,
+                                             "aggregate_GB/s": world * nb / ms / 1e6,
+                                             "nvlink_frac": nb / ms / 1e6 / NVLINK_PEER_GBS}
+            mp.release_prefix(nd)
+        res["sweep"] = pairs
+        res["nvlink_peak"] = {"GB/s": NVLINK_PEER_GBS, "source": "measured peer copy per direction "
+                              "(B200_PROFILING.md; 900 nominal)"}
+    if decode_step is not None:
+        res["overlap"] = measure_overlap(mp, wl, world, rank, dev, torch, dist, decode_step)
+    torch.cuda.synchronize()
+    mp.destroy()
+    if decode_step is not None:
+        # the same with the migration's SM share bounded (NCCL maxCTAs, copy-kernel CTAs)
+        cfg = {"max_ctas": 2, "copy_ctas": 2 * 148}
+        mp = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, 2 * 512 + 64, dev)
+        uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
+        if world > 1:
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        mp.comm_init(uid, world, rank, **cfg)
+        res["overlap_bounded"] = dict(measure_overlap(mp, wl, world, rank, dev, torch, dist, decode_step),
+                                      comm_config=cfg)
         torch.cuda.synchronize()
-        src.destroy()
-        dst.destroy()
-        res["sweep"] = sweep
-        return res
-    uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
-    obj = [uid]
-    dist.broadcast_object_list(obj, src=0)
-    pool.comm_init(obj[0], world, rank)
-    res = {}
-    for it in range(3):
+        mp.destroy()
+    return res
+
+
+def _ranked_timed(fn, stream, torch, dist, dev, reps=3):
+    """Best of `reps` (barrier; events around fn on `stream`; max over ranks)."""
+    best = None
+    for it in range(reps + 1):
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        newn = None
-        if rank == 0:
-            pool.migrate_send(node, 1, 1)
-        elif rank == 1:
-            newn = pool.migrate_recv(0, -1, ntok)
-        e1.record()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
         torch.cuda.synchronize()
         ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{dev}")
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        if newn is not None:
-            pool.release_prefix(newn)
-        gbs = nbytes / ms.item() / 1e6
-        res = {"mode": "rank0 -> rank1 NCCL send/recv (COPY), K4 pack/unpack pipelined",
-               "bytes": nbytes, "ms": ms.item(), "GB/s": gbs,
-               "nvlink_roofline": {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_PEER_GBS,
-                                   "unit": "GB/s", "frac": gbs / NVLINK_PEER_GBS,
-                                   "peak_source": "measured peer copy per direction "
-                                                  "(B200_PROFILING.md; 900 nominal)"}}
-    return res
+        if it > 0:  # the first call connects the peers
+            best = ms.item() if best is None else min(best, ms.item())
+    return best
+
+
+def measure_overlap(mp, wl, world, rank, dev, torch, dist, decode_step, ntok=8192, dec_steps=20):
+    """Migration on a side stream while C1 decode steps run on the compute stream (the
+    deployment the paper describes: snapshots move under scheduler control while decode
+    continues; compute-communication overlap, :9, :59).  Three passes: decode
+    alone, migration alone, both (the migration loop sized to span the decode pass).  N=1:
+    loopback (both ends on this GPU: the worst case for HBM contention); N>1: ring
+    permutation.  NCCL CTAs / copy CTAs are the communicator's defaults."""
+    compute = torch.cuda.current_stream()
+    side = torch.cuda.Stream(device=f"cuda:{dev}")
+    kx = torch.empty((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
+    kx.normal_()
+    nd = mp.register_prefix(-1, ntok, kx, kx, compute)
+    del kx
+    nb = _node_bytes(wl, ntok)
+    dst, src = (rank + 1) % world, (rank - 1) % world
+
+    def migrate():
+        (n2,) = mp.migrate_exchange(sends=[(nd, dst, 1)], recvs=[(src, -1, ntok)], stream=side)
+        mp.release_prefix(n2)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def span(events):
+        return events[0].elapsed_time(events[1])
+
+    for _ in range(3):
+        decode_step()
+        migrate()
+    sync_all()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(compute)
+    for _ in range(dec_steps):
+        decode_step()
+    ev[1].record(compute)
+    sync_all()
+    dec_alone = span(ev)
+    ev[0].record(side)
+    migrate()
+    ev[1].record(side)
+    sync_all()
+    mig_one = span(ev)
+    reps = max(1, int(round(dec_alone / mig_one)))
+    evm = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(side)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        migrate()
+    host_ms = (time.perf_counter() - t0) * 1e3 / reps
+    ev[1].record(side)
+    sync_all()
+    mig_alone = span(ev)
+    # both: the host interleaves the enqueues (migrations spread evenly over the decode steps)
+    # so the two streams really run side by side on the GPU
+    evm[0].record(side)
+    ev[0].record(compute)
+    done = 0
+    for i in range(dec_steps):
+        decode_step()
+        while done < reps * (i + 1) // dec_steps:
+            migrate()
+            done += 1
+    ev[1].record(compute)
+    evm[1].record(side)
+    sync_all()
+    dec_both, mig_both = span(ev), span(evm)
+    vals = [dec_alone, dec_both, mig_alone, mig_both]
+    if world > 1:
+        from paper_2509_02121_b200.sharding import max_over_ranks
+        vals = max_over_ranks(vals, dist, f"cuda:{dev}")
+    dec_alone, dec_both, mig_alone, mig_both = vals
+    mp.release_prefix(nd)
+    return {"what": (f"{reps} x {ntok}-token node ({nb >> 20} MiB K+V) migrations on a side stream "
+                     f"{'(loopback)' if world == 1 else '(ring permutation)'} concurrent with "
+                     f"{dec_steps} C1 decode steps on the compute stream"),
+            "decode_ms_per_step_alone": dec_alone / dec_steps,
+            "decode_ms_per_step_with_migration": dec_both / dec_steps,
+            "decode_slowdown_pct": 100.0 * (dec_both / dec_alone - 1.0),
+            "migration_GB/s_alone": reps * nb / mig_alone / 1e6,
+            "migration_GB/s_with_decode": reps * nb / mig_both / 1e6,
+            "migration_ms_alone": mig_alone, "migration_ms_with_decode": mig_both,
+            "host_enqueue_ms_per_migration": host_ms}
 
 
 if __name__ == "__main__":

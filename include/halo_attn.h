@@ -70,7 +70,11 @@ int32_t halo_abi_version(void);
  * layout of each of K and V (bf16):
  *     [layer][block][kv_head][16][head_dim]
  * so one (block, kv_head) slab is 16*head_dim*2 bytes contiguous (4 KiB at d=128).
- * (Block-level KV management as in vLLM, §4.1 Baselines.) */
+ * (Block-level KV management as in vLLM, §4.1 Baselines.)
+ * Value domain: any finite bf16 K and V.  (The prefix kernel multiplies V by an exact power
+ * of two per tile before its fp16 P.V MMA so that V beyond fp16's range neither overflows nor
+ * loses precision; inf / nan inputs propagate.)  The library zero-fills the pool at creation
+ * (caller storage included), so never-written slots hold finite values. */
 typedef struct {
     int32_t device;          /* CUDA ordinal.  -1 = host-only bookkeeping: no device
                                 memory, no launches (used to test allocator/tree/plan on

@@ -77,7 +77,15 @@ struct PlanDev {
 struct PoolGeom {
     int32_t layers, hkv, hq, d;
     int64_t cap;  // blocks per layer
+    // V magnitude table [layer][block]: (allocation epoch of the block << 16) | bf16 bits of
+    // max |V| over the block's written tokens (all kv heads).  Writers of a block store or
+    // atomicMax with the block's epoch, so entries left by a previous owner lose to the
+    // current owner's first write.  Read by K1 to pick its per-tile fp16 scale for V.
+    uint64_t *vmax;
 };
+__host__ __device__ inline uint64_t vmax_entry(uint32_t epoch, uint32_t maxbits) {
+    return ((uint64_t)epoch << 16) | (maxbits & 0xffffu);
+}
 
 // ---- launchers (kernels_*.cu) ----
 // K1: tcgen05/TMEM prefix attention -> normalised fp32 partials + lse (natural log).
@@ -93,10 +101,11 @@ cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void
                                  float *lse, float scale, int num_sms, cudaStream_t s);
 // K5 / K4-unpack: rows src[layer][i][head][:] -> pool slot slots[i] (i < n_copy); slots
 // [n_copy, n_copy+n_zero) are zero-filled.  src has `src_rows` rows per layer.
+// tags[i] (nullable: no V-table update) = allocation epoch of slot i's block.
 cudaError_t launch_kv_scatter(const PoolGeom &g, void *pool_k, void *pool_v, const void *src_k,
                               const void *src_v, int64_t src_rows, const int32_t *slots,
-                              int64_t n_copy, int64_t n_zero, int layer_begin, int layer_end,
-                              int num_sms, cudaStream_t s);
+                              const uint32_t *tags, int64_t n_copy, int64_t n_zero, int layer_begin,
+                              int layer_end, int num_sms, cudaStream_t s);
 // K4 pack: pool slot slots[i] -> dst[layer - layer_begin][i][head][:], i < n.
 cudaError_t launch_kv_gather(const PoolGeom &g, const void *pool_k, const void *pool_v,
                              void *dst_k, void *dst_v, const int32_t *slots, int64_t n,
@@ -105,17 +114,25 @@ cudaError_t launch_kv_gather(const PoolGeom &g, const void *pool_k, const void *
 // Same-device relocation: pool block pairs[2i] -> destination block pairs[2i+1], all
 // layers in [layer_begin, layer_end), K and V (whole blocks: a partial block's zero tail
 // is copied as well).
+// dst_tags[i] = allocation epoch of destination block pairs[2i+1] (its V-table entry is the
+// source entry's max with this epoch).
 cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const void *src_v,
                                   const PoolGeom &dg, void *dst_k, void *dst_v,
-                                  const int32_t *pairs, int32_t nblk, int layer_begin,
-                                  int layer_end, int num_sms, cudaStream_t s);
+                                  const int32_t *pairs, const uint32_t *dst_tags, int32_t nblk,
+                                  int layer_begin, int layer_end, int num_sms, cudaStream_t s);
+// V-table entries of blocks[0..nblk) x layers [0, layers) recomputed from the pool's V (after a
+// copy-engine write, e.g. a host-arena fetch); tags[i] = epoch of blocks[i].
+cudaError_t launch_kv_vmax(const PoolGeom &g, const void *pool_v, const int32_t *blocks,
+                           const uint32_t *tags, int32_t nblk, int num_sms, cudaStream_t s);
 
 // Migration K4 pack (to_pool = false) / unpack (true), block-granular: items
 // [item_begin, item_end) of the node's flattened [layer][block] list (layer = j / nblk,
 // pool block blocks[j % nblk]); wire layout [item][K|V][hkv][16][d] bf16.  At most max_ctas
 // CTAs of 256 threads (bounded so a migration can run beside decode).
+// Unpack also writes the V-table entries of the blocks it fills (tags[j % nblk] = epoch).
 cudaError_t launch_kv_runs(const PoolGeom &g, void *pool_k, void *pool_v, void *buf,
-                           const int32_t *blocks, int32_t nblk, int64_t item_begin,
-                           int64_t item_end, bool to_pool, int max_ctas, cudaStream_t s);
+                           const int32_t *blocks, const uint32_t *tags, int32_t nblk,
+                           int64_t item_begin, int64_t item_end, bool to_pool, int max_ctas,
+                           cudaStream_t s);
 
 }  // namespace halo

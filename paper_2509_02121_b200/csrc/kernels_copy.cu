@@ -11,6 +11,8 @@
 // of the SM count.
 #include "halo_internal.h"
 
+#include <algorithm>
+
 namespace halo {
 namespace {
 
@@ -22,6 +24,28 @@ __device__ __forceinline__ int4 ld_stream(const int4 *p) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
+}
+
+// bf16 bits of max |x| over the 8 bf16 of a 16-B chunk (magnitude bits order like the values).
+__device__ __forceinline__ uint32_t absmax8(int4 w) {
+    const uint32_t a = max(max((uint32_t)w.x & 0x7fffu, ((uint32_t)w.x >> 16) & 0x7fffu),
+                           max((uint32_t)w.y & 0x7fffu, ((uint32_t)w.y >> 16) & 0x7fffu));
+    const uint32_t b = max(max((uint32_t)w.z & 0x7fffu, ((uint32_t)w.z >> 16) & 0x7fffu),
+                           max((uint32_t)w.w & 0x7fffu, ((uint32_t)w.w >> 16) & 0x7fffu));
+    return max(a, b);
+}
+
+// Block-wide max of m (256 threads), valid in thread 0.
+__device__ __forceinline__ uint32_t cta_max256(uint32_t m) {
+    __shared__ uint32_t red[8];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int i = 1; i < 8; ++i) m = max(m, red[i]);
+    __syncthreads();
+    return m;
 }
 
 struct Geo {
@@ -42,8 +66,9 @@ __device__ __forceinline__ int64_t pool_chunk(const Geo &g, int layer, int32_t s
 // src/dst exchange rows: [layer][i][h][chunk]
 __global__ void kv_scatter_kernel(int4 *__restrict__ pk, int4 *__restrict__ pv,
                                   const int4 *__restrict__ sk, const int4 *__restrict__ sv,
-                                  Geo g, const int32_t *__restrict__ slots, int64_t n_copy,
-                                  int layer_begin) {
+                                  Geo g, const int32_t *__restrict__ slots,
+                                  const uint32_t *__restrict__ tags, uint64_t *__restrict__ vmax,
+                                  int64_t cap, int64_t n_copy, int layer_begin) {
     const int inner = g.hkv * g.cpr;
     const int lane_tok = threadIdx.x / inner;
     if (lane_tok >= g.tpb) return;
@@ -75,6 +100,20 @@ __global__ void kv_scatter_kernel(int4 *__restrict__ pk, int4 *__restrict__ pv,
             if (dst[u] >= 0) {
                 pk[dst[u]] = vk[u];
                 pv[dst[u]] = vv[u];
+            }
+        }
+        if (tags) {  // V-table: max |V| per (layer, block), lanes of one block reduced first
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int64_t i = i0 + u * step;
+                const int32_t blk = i < g.n ? (slots[i] >> 4) : -1;
+                const uint32_t m = blk >= 0 ? absmax8(vv[u]) : 0u;
+                const uint32_t act = __activemask();
+                const uint32_t grp = __match_any_sync(act, blk);
+                const uint32_t red = __reduce_max_sync(grp, m);
+                if (blk >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1)
+                    atomicMax(reinterpret_cast<unsigned long long *>(vmax + (int64_t)layer * cap + blk),
+                              (unsigned long long)vmax_entry(tags[i], red));
             }
         }
     }
@@ -139,8 +178,10 @@ void shape(const PoolGeom &pg, int64_t n, int layers, int num_sms, Geo &g, dim3 
 constexpr int kCopyUnroll = 8;
 __global__ void __launch_bounds__(256) kv_copy_blocks_kernel(
     const int4 *__restrict__ sk, const int4 *__restrict__ sv, int4 *__restrict__ dk,
-    int4 *__restrict__ dv, const int32_t *__restrict__ pairs, int64_t nitems, int32_t nblk,
-    int32_t run16, int64_t src_layer16, int64_t dst_layer16, int layer_begin) {
+    int4 *__restrict__ dv, const int32_t *__restrict__ pairs, const uint32_t *__restrict__ dst_tags,
+    const uint64_t *__restrict__ src_vmax, uint64_t *__restrict__ dst_vmax, int64_t src_cap,
+    int64_t dst_cap, int64_t nitems, int32_t nblk, int32_t run16, int64_t src_layer16,
+    int64_t dst_layer16, int layer_begin) {
     // item = ((layer - layer_begin) * nblk + pair) * 2 + (K|V): one contiguous run of run16 int4
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         const int kv = (int)(item & 1);
@@ -149,6 +190,9 @@ __global__ void __launch_bounds__(256) kv_copy_blocks_kernel(
         const int64_t layer = layer_begin + lp / nblk;
         const int4 *src = (kv ? sv : sk) + layer * src_layer16 + (int64_t)pairs[2 * pr] * run16;
         int4 *dst = (kv ? dv : dk) + layer * dst_layer16 + (int64_t)pairs[2 * pr + 1] * run16;
+        if (kv && threadIdx.x == 0)
+            dst_vmax[layer * dst_cap + pairs[2 * pr + 1]] =
+                vmax_entry(dst_tags[pr], (uint32_t)src_vmax[layer * src_cap + pairs[2 * pr]]);
         for (int o0 = threadIdx.x; o0 < run16; o0 += 256 * kCopyUnroll) {
             int4 v[kCopyUnroll];
 #pragma unroll
@@ -168,8 +212,9 @@ __global__ void __launch_bounds__(256) kv_copy_blocks_kernel(
 // last block included, so the destination slab is bit-identical to the source slab.
 __global__ void __launch_bounds__(256) kv_runs_kernel(
     int4 *__restrict__ pk, int4 *__restrict__ pv, int4 *__restrict__ buf,
-    const int32_t *__restrict__ blocks, int32_t nblk, int64_t item_begin, int64_t nitems2,
-    int32_t run16, int64_t pool_layer16, int to_pool) {
+    const int32_t *__restrict__ blocks, const uint32_t *__restrict__ tags, uint64_t *__restrict__ vmax,
+    int64_t cap, int32_t nblk, int64_t item_begin, int64_t nitems2, int32_t run16,
+    int64_t pool_layer16, int to_pool) {
     for (int64_t it = blockIdx.x; it < nitems2; it += gridDim.x) {
         const int kv = (int)(it & 1);
         const int64_t j = item_begin + (it >> 1);
@@ -178,6 +223,7 @@ __global__ void __launch_bounds__(256) kv_runs_kernel(
         int4 *wire = buf + it * run16;
         const int4 *src = to_pool ? wire : pool;
         int4 *dst = to_pool ? pool : wire;
+        uint32_t m = 0;
         for (int o0 = threadIdx.x; o0 < run16; o0 += 256 * kCopyUnroll) {
             int4 v[kCopyUnroll];
 #pragma unroll
@@ -185,8 +231,30 @@ __global__ void __launch_bounds__(256) kv_runs_kernel(
                 if (o0 + u * 256 < run16) v[u] = ld_stream(src + o0 + u * 256);
 #pragma unroll
             for (int u = 0; u < kCopyUnroll; ++u)
-                if (o0 + u * 256 < run16) dst[o0 + u * 256] = v[u];
+                if (o0 + u * 256 < run16) {
+                    dst[o0 + u * 256] = v[u];
+                    m = max(m, absmax8(v[u]));
+                }
         }
+        if (to_pool && kv) {  // the block's V-table entry (a whole block arrived)
+            m = cta_max256(m);
+            if (threadIdx.x == 0) vmax[layer * cap + blocks[j % nblk]] = vmax_entry(tags[j % nblk], m);
+        }
+    }
+}
+
+// V-table entries recomputed from the pool: one CTA per (layer, block).
+__global__ void __launch_bounds__(256) kv_vmax_kernel(const int4 *__restrict__ pv, const int32_t *__restrict__ blocks,
+                                                      const uint32_t *__restrict__ tags, uint64_t *__restrict__ vmax,
+                                                      int64_t cap, int32_t nblk, int64_t nitems, int32_t run16) {
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int64_t layer = it / nblk;
+        const int32_t b = blocks[it % nblk];
+        const int4 *src = pv + (layer * cap + b) * run16;
+        uint32_t m = 0;
+        for (int o = threadIdx.x; o < run16; o += 256) m = max(m, absmax8(ld_stream(src + o)));
+        m = cta_max256(m);
+        if (threadIdx.x == 0) vmax[layer * cap + b] = vmax_entry(tags[it % nblk], m);
     }
 }
 
@@ -194,8 +262,8 @@ __global__ void __launch_bounds__(256) kv_runs_kernel(
 
 cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const void *src_v,
                                   const PoolGeom &dg, void *dst_k, void *dst_v,
-                                  const int32_t *pairs, int32_t nblk, int layer_begin,
-                                  int layer_end, int num_sms, cudaStream_t s) {
+                                  const int32_t *pairs, const uint32_t *dst_tags, int32_t nblk,
+                                  int layer_begin, int layer_end, int num_sms, cudaStream_t s) {
     const int layers = layer_end - layer_begin;
     if (nblk == 0 || layers <= 0) return cudaSuccess;
     const int32_t run16 = sg.hkv * kBlockTok * sg.d * 2 / 16;  // int4 chunks per (layer, block)
@@ -204,15 +272,16 @@ cudaError_t launch_kv_copy_blocks(const PoolGeom &sg, const void *src_k, const v
     const int64_t cap = (int64_t)num_sms * 8;  // 8 CTAs of 256 threads per SM
     if (grid > cap) grid = cap;
     kv_copy_blocks_kernel<<<(unsigned)grid, 256, 0, s>>>(
-        (const int4 *)src_k, (const int4 *)src_v, (int4 *)dst_k, (int4 *)dst_v, pairs, nitems,
-        nblk, run16, sg.cap * run16, dg.cap * run16, layer_begin);
+        (const int4 *)src_k, (const int4 *)src_v, (int4 *)dst_k, (int4 *)dst_v, pairs, dst_tags,
+        sg.vmax, dg.vmax, sg.cap, dg.cap, nitems, nblk, run16, sg.cap * run16, dg.cap * run16,
+        layer_begin);
     return cudaGetLastError();
 }
 
 cudaError_t launch_kv_scatter(const PoolGeom &pg, void *pool_k, void *pool_v, const void *src_k,
                               const void *src_v, int64_t src_rows, const int32_t *slots,
-                              int64_t n_copy, int64_t n_zero, int layer_begin, int layer_end,
-                              int num_sms, cudaStream_t s) {
+                              const uint32_t *tags, int64_t n_copy, int64_t n_zero, int layer_begin,
+                              int layer_end, int num_sms, cudaStream_t s) {
     const int64_t n = n_copy + n_zero;
     const int layers = layer_end - layer_begin;
     if (n == 0 || layers <= 0) return cudaSuccess;
@@ -223,7 +292,7 @@ cudaError_t launch_kv_scatter(const PoolGeom &pg, void *pool_k, void *pool_v, co
     g.src_rows = src_rows;
     kv_scatter_kernel<<<grid, threads, 0, s>>>((int4 *)pool_k, (int4 *)pool_v,
                                                (const int4 *)src_k, (const int4 *)src_v, g,
-                                               slots, n_copy, layer_begin);
+                                               slots, tags, pg.vmax, pg.cap, n_copy, layer_begin);
     return cudaGetLastError();
 }
 
@@ -244,16 +313,28 @@ cudaError_t launch_kv_gather(const PoolGeom &pg, const void *pool_k, const void 
 }
 
 cudaError_t launch_kv_runs(const PoolGeom &pg, void *pool_k, void *pool_v, void *buf,
-                           const int32_t *blocks, int32_t nblk, int64_t item_begin,
-                           int64_t item_end, bool to_pool, int max_ctas, cudaStream_t s) {
+                           const int32_t *blocks, const uint32_t *tags, int32_t nblk,
+                           int64_t item_begin, int64_t item_end, bool to_pool, int max_ctas,
+                           cudaStream_t s) {
     const int64_t nitems2 = 2 * (item_end - item_begin);
     if (nblk == 0 || nitems2 <= 0) return cudaSuccess;
     const int32_t run16 = pg.hkv * kBlockTok * pg.d * 2 / 16;
     int64_t grid = nitems2;
     if (grid > max_ctas) grid = max_ctas;
-    kv_runs_kernel<<<(unsigned)grid, 256, 0, s>>>((int4 *)pool_k, (int4 *)pool_v, (int4 *)buf, blocks,
-                                                  nblk, item_begin, nitems2, run16, pg.cap * run16,
-                                                  to_pool ? 1 : 0);
+    kv_runs_kernel<<<(unsigned)grid, 256, 0, s>>>((int4 *)pool_k, (int4 *)pool_v, (int4 *)buf, blocks, tags,
+                                                  pg.vmax, pg.cap, nblk, item_begin, nitems2, run16,
+                                                  pg.cap * run16, to_pool ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kv_vmax(const PoolGeom &pg, const void *pool_v, const int32_t *blocks,
+                           const uint32_t *tags, int32_t nblk, int num_sms, cudaStream_t s) {
+    const int64_t nitems = (int64_t)pg.layers * nblk;
+    if (nitems == 0) return cudaSuccess;
+    const int32_t run16 = pg.hkv * kBlockTok * pg.d * 2 / 16;
+    int64_t grid = std::min<int64_t>(nitems, (int64_t)num_sms * 8);
+    kv_vmax_kernel<<<(unsigned)grid, 256, 0, s>>>((const int4 *)pool_v, blocks, tags, pg.vmax, pg.cap, nblk,
+                                                  nitems, run16);
     return cudaGetLastError();
 }
 

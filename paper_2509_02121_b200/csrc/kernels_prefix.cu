@@ -29,12 +29,19 @@
 //               versa.  tcgen05.mma executes in issue order, so QK_X(n) may overwrite the
 //               S/P columns PV_X(n-1) reads.
 //   warps 10-11 V converters: bf16 -> fp16 in place on each V stage (fp16 P needs fp16 V:
-//               kind::f16 takes A and B in one format; reading R8).
+//               kind::f16 takes A and B in one format; reading R8), scaled by an
+//               exact power of two 2^-s per tile so that any finite bf16 V fits fp16's range.
+//               s comes from the pool's V table (max |V| per (layer, block), maintained by
+//               every kernel that writes pool blocks): s = 0 while the tile's max |V| is in
+//               [2^-4, 2^15), else (exponent of max) - 14, so converted values stay < 2^15 and
+//               those >= max * 2^-29 stay fp16-normal; the epilogue multiplies by 2^s.  Powers of
+//               two are exact: for in-range V nothing changes (K1, "V range").
 //
 // TMEM columns: S_A/P_A [0,128) | S_B/P_B [128,256) | O_A [256,256+d) | O_B [384,384+d).
 #include "halo_internal.h"
 #include "ptx.h"
 
+#include <cuda_bf16.h>
 #include <cstdlib>
 
 #ifdef HALO_K1_TRACE
@@ -73,6 +80,8 @@ struct PrefixArgs {
     int64_t layer_blk;  // layer * cap (4th TMA coordinate offset)
     float qscale;       // scale * log2(e)
     int32_t tma_q;      // tmq is valid: tiles with consecutive requests load Q by TMA
+    const uint64_t *vmax;  // the pool's V table [layer][block] (low 16 bits: bf16 max |V|)
+    int64_t cap;
 };
 
 template <int D>
@@ -90,7 +99,9 @@ struct L1 {
     static constexpr int NBAR = 40;
     static constexpr int OFF_BLK = OFF_BAR + NBAR * 8 + 16;       // block ids of the tile range
     static constexpr int MAX_BLK = kK1MaxTileTok / kBlockTok;
-    static constexpr int SMEM = OFF_BLK + MAX_BLK * 4;              // base must be 1024-aligned
+    static constexpr int OFF_VEXP = OFF_BLK + MAX_BLK * 4;          // the tile's V scale exponent
+    static constexpr int OFF_VRED = OFF_VEXP + 4 * 4;               // [2 warps] V max reduction
+    static constexpr int SMEM = OFF_VRED + 4 * 4;                   // base must be 1024-aligned
     static constexpr int O_STRIDE = D * 4;                          // epilogue staging row bytes
     static __host__ __device__ constexpr uint32_t tmem_s(int x) { return x ? 128u : 0u; }
     static __host__ __device__ constexpr uint32_t tmem_o(int x) { return x ? 384u : 256u; }
@@ -108,6 +119,48 @@ enum Bar {
                                                  // pass; index EXP_DONE + 4 x + w (w = warp & 3)
 
 };
+
+// TMA loads of n-tile n of tile T (128 tokens = 8 paged blocks) of K or V into `dst`, completing
+// on `full` (expect_tx armed here): one 4-D box per d atom when the 8 blocks are physically
+// consecutive, else one per block; blocks past the tile's end re-load a valid block (their
+// scores are masked).  blocks = the tile's block ids from blk_first on (smem).
+template <int D>
+__device__ __forceinline__ void issue_kv_tile(const CUtensorMap *map, const CUtensorMap *map8, uint8_t *dst,
+                                              uint64_t *full, const int32_t *blocks, const PrefixTile &T,
+                                              int blk_first, int n, int64_t layer_blk) {
+    using C = L1<D>;
+    const int tok0 = T.tok_begin + n * kK1Tok;
+    const int nb = (min(kK1Tok, T.tok_end - tok0) + kBlockTok - 1) / kBlockTok;
+    const int blk0 = tok0 / kBlockTok - blk_first;
+    ptx::mbar_arrive_expect_tx(full, C::KV_BYTES);
+    const int b0 = blocks[blk0];
+    bool contiguous = nb == kK1Tok / kBlockTok;
+#pragma unroll
+    for (int bi = 1; bi < kK1Tok / kBlockTok; ++bi)
+        contiguous &= (bi >= nb) || blocks[blk0 + bi] == b0 + bi;
+    if (contiguous) {  // physically consecutive blocks: one 128-token box per d atom
+        for (int at = 0; at < C::ATOMS; ++at)
+            ptx::tma_load_4d(dst + at * C::ATOM_BYTES, map8, at * 64, 0, T.kv_head, (int)(layer_blk + b0), full);
+        return;
+    }
+    for (int bi = 0; bi < kK1Tok / kBlockTok; ++bi) {
+        const int blk = blocks[blk0 + (bi < nb ? bi : 0)];
+        for (int at = 0; at < C::ATOMS; ++at)
+            ptx::tma_load_4d(dst + at * C::ATOM_BYTES + bi * kBlockTok * 128, map, at * 64, 0, T.kv_head,
+                             (int)(layer_blk + blk), full);
+    }
+}
+
+// bf16 pair -> fp16 pair scaled by sc (an exact power of two; unit: no multiply).  satfinite:
+// stale values in the masked tail of a suffix block can never become inf (P = 0 there, and
+// 0 x inf would be nan).
+__device__ __forceinline__ uint32_t cvt_v2(uint32_t w, float2 scv, bool unit) {
+    float2 f = ptx::bf2_to_f2(w);
+    if (!unit) f = ptx::fmul2(f, scv);
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(f.y), "f"(f.x));
+    return r;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -201,28 +254,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
                 }
             }
             auto issue = [&](const CUtensorMap *map, const CUtensorMap *map8, uint8_t *dst, uint64_t *full, int n) {
-                const int tok0 = T.tok_begin + n * kK1Tok;
-                const int nb = (min(kK1Tok, T.tok_end - tok0) + kBlockTok - 1) / kBlockTok;
-                const int blk0 = tok0 / kBlockTok - blk_first;
-                ptx::mbar_arrive_expect_tx(full, C::KV_BYTES);
-                const int b0 = blocks[blk0];
-                bool contiguous = nb == kK1Tok / kBlockTok;
-#pragma unroll
-                for (int bi = 1; bi < kK1Tok / kBlockTok; ++bi)
-                    contiguous &= (bi >= nb) || blocks[blk0 + bi] == b0 + bi;
-                if (contiguous) {  // physically consecutive blocks: one 128-token box per d atom
-                    for (int at = 0; at < C::ATOMS; ++at)
-                        ptx::tma_load_4d(dst + at * C::ATOM_BYTES, map8, at * 64, 0, T.kv_head,
-                                         (int)(a.layer_blk + b0), full);
-                    return;
-                }
-                for (int bi = 0; bi < kK1Tok / kBlockTok; ++bi) {
-                    // blocks past the tile's end re-load a valid block; their scores are masked
-                    const int blk = blocks[blk0 + (bi < nb ? bi : 0)];
-                    for (int at = 0; at < C::ATOMS; ++at)
-                        ptx::tma_load_4d(dst + at * C::ATOM_BYTES + bi * kBlockTok * 128, map,
-                                         at * 64, 0, T.kv_head, (int)(a.layer_blk + blk), full);
-                }
+                issue_kv_tile<D>(map, map8, dst, full, blocks, T, blk_first, n, a.layer_blk);
             };
             int nk = 0, nv = 0;
             while (nk < NT || nv < NT) {
@@ -293,26 +325,62 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         }
     } else if (warp >= 10) {
         HALO_REGS_DEC();
-        // ===================== V converters: bf16 -> fp16 in place =====================
+        // ===================== V converters: bf16 -> fp16 in place, scaled =====================
         const int t = threadIdx.x - 320;  // 0..63
-        for (int n = 0; n < NT; ++n) {
-            const int st = n % SV;
-            ptx::mbar_wait(&bar[V_FULL + st], (n / SV) & 1);
-            if (t == 0) K1_TRACE(4, n);
-            uint4 *vs = reinterpret_cast<uint4 *>(sm + C::OFF_V + st * C::KV_BYTES);
-#pragma unroll 4
-            for (int c = t; c < C::KV_BYTES / 16; c += 64) {
-                uint4 w = vs[c];
-                float2 f;
-                f = ptx::bf2_to_f2(w.x); w.x = ptx::f2_to_h2(f.x, f.y);
-                f = ptx::bf2_to_f2(w.y); w.y = ptx::f2_to_h2(f.x, f.y);
-                f = ptx::bf2_to_f2(w.z); w.z = ptx::f2_to_h2(f.x, f.y);
-                f = ptx::bf2_to_f2(w.w); w.w = ptx::f2_to_h2(f.x, f.y);
-                vs[c] = w;
+        int32_t *vexp = reinterpret_cast<int32_t *>(sm + C::OFF_VEXP);
+        uint32_t *vred = reinterpret_cast<uint32_t *>(sm + C::OFF_VRED);
+        // the tile's scale: max over its blocks' V-table entries (written by earlier kernels)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        {
+            const int blk_first = T.tok_begin / kBlockTok;
+            const int nblk = (T.tok_end + kBlockTok - 1) / kBlockTok - blk_first;
+            const uint64_t *vrow = a.vmax + (a.layer_blk / a.cap) * a.cap;
+            uint32_t mx = 0;
+            for (int i = t; i < nblk; i += 64) {
+                const int blk = aux.y >= 0 ? aux.y + i : a.p.node_blocks[T.blk_off + blk_first + i];
+                mx = max(mx, (uint32_t)vrow[blk] & 0xffffu);
             }
-            ptx::fence_proxy_async_smem();
-            if (t == 0) K1_TRACE(5, n);
-            ptx::mbar_arrive(&bar[V_CONV + st]);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) vred[warp - 10] = mx;
+            asm volatile("bar.sync 3, 64;" ::: "memory");
+            mx = min(max(vred[0], vred[1]), 0x7f7fu);  // inf / nan -> max finite
+            const int E = (int)(mx >> 7) - 127;        // floor(log2 max |V|)
+            const int s = (mx != 0 && (E >= 15 || E < -4)) ? max(E - 14, -100) : 0;
+            if (t == 0) vexp[0] = s;
+            const bool unit = s == 0;
+            const float sc = __uint_as_float((uint32_t)(127 - s) << 23);  // 2^-s, exact
+            const float2 scv = make_float2(sc, sc);
+            for (int n = 0; n < NT; ++n) {
+                const int st = n % SV;
+                ptx::mbar_wait(&bar[V_FULL + st], (n / SV) & 1);
+                if (t == 0) K1_TRACE(4, n);
+                uint4 *vs = reinterpret_cast<uint4 *>(sm + C::OFF_V + st * C::KV_BYTES);
+                if (unit) {
+#pragma unroll 4
+                    for (int c = t; c < C::KV_BYTES / 16; c += 64) {
+                        uint4 w = vs[c];
+                        w.x = cvt_v2(w.x, scv, true);
+                        w.y = cvt_v2(w.y, scv, true);
+                        w.z = cvt_v2(w.z, scv, true);
+                        w.w = cvt_v2(w.w, scv, true);
+                        vs[c] = w;
+                    }
+                } else {
+#pragma unroll 4
+                    for (int c = t; c < C::KV_BYTES / 16; c += 64) {
+                        uint4 w = vs[c];
+                        w.x = cvt_v2(w.x, scv, false);
+                        w.y = cvt_v2(w.y, scv, false);
+                        w.z = cvt_v2(w.z, scv, false);
+                        w.w = cvt_v2(w.w, scv, false);
+                        vs[c] = w;
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                if (t == 0) K1_TRACE(5, n);
+                ptx::mbar_arrive(&bar[V_CONV + st]);
+            }
         }
     } else {
         HALO_REGS_INC();
@@ -351,7 +419,9 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         const uint32_t s_addr = lane_addr + C::tmem_s(x);
         const uint32_t o_addr = lane_addr + C::tmem_o(x);
         const float c2 = a.qscale;
+        const int32_t *vexp = reinterpret_cast<const int32_t *>(sm + C::OFF_VEXP);
         float m_ref = -INFINITY, l = 0.f;
+        int s_cur = 0;  // the tile's V scale exponent: O accumulates P.(V 2^-s)
         for (int n = 0; n < NT; ++n) {
             ptx::mbar_wait(&bar[S_FULL + x], n & 1);
             if (threadIdx.x == 0) K1_TRACE(6, n);
@@ -439,6 +509,10 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             if (hasB) ptx::mbar_arrive(&bar[EXP_DONE + 4 * x + wq]);
             if (threadIdx.x == 0) K1_TRACE(11, n);
             if (threadIdx.x == 128) K1_TRACE(13, n);
+            if (n == 0) {  // the tile's V scale (set by the converters before their first arrive)
+                ptx::mbar_wait(&bar[V_CONV], 0);
+                s_cur = vexp[0];
+            }
             ptx::tmem_wait_st();
             if (threadIdx.x == 0) K1_TRACE(8, n);
             ptx::tc_fence_before();
@@ -447,7 +521,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         // ---- epilogue: O / l -> normalised partial, lse ----
         ptx::mbar_wait(&bar[PV_DONE + x], (NT - 1) & 1);
         ptx::tc_fence_after();
-        const float inv = 1.f / l;
+        const float inv = (1.f / l) * __uint_as_float((uint32_t)(127 + s_cur) << 23);  // x 2^s: exact
         // staging: sub-tile A in the K ring, B in the V ring (both idle once PV_x(NT-1) is done);
         // row r's 16-B chunks XOR-swizzled by row
         uint8_t *stage = sm + (x == 0 ? C::OFF_K : C::OFF_V);
@@ -535,6 +609,8 @@ cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tma
     a.layer_blk = (int64_t)layer * g.cap;
     a.qscale = scale * kLog2e;
     a.tma_q = tmap_q != nullptr ? 1 : 0;
+    a.vmax = g.vmax;
+    a.cap = g.cap;
     const CUtensorMap *tq = tmap_q != nullptr ? tmap_q : tmap_k;  // unused when tma_q == 0
     if (g.d == 128) return launch_t<128>(tmap_k, tmap_v, tmap_k8, tmap_v8, tq, a, s);
     if (g.d == 64) return launch_t<64>(tmap_k, tmap_v, tmap_k8, tmap_v8, tq, a, s);

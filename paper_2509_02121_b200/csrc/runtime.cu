@@ -196,11 +196,25 @@ halo_status alloc_blocks(halo_pool p, int64_t n, std::vector<int32_t> &out) {
         return fail(HALO_ENOMEM, "pool out of blocks: need %lld, free %lld", (long long)n,
                     (long long)p->free_list.size());
     out.reserve(out.size() + n);
+    ++p->epoch;  // a new owner: its V-table writes outrank every earlier owner's
     for (int64_t i = 0; i < n; ++i) {
         out.push_back(p->free_list.back());
+        p->blk_epoch[out.back()] = p->epoch;
         p->free_list.pop_back();
     }
     return HALO_OK;
+}
+
+// Allocation epochs of the blocks of `slots` (token slots) or of `blocks`.
+std::vector<uint32_t> slot_tags(halo_pool p, const std::vector<int32_t> &slots) {
+    std::vector<uint32_t> t(slots.size());
+    for (size_t i = 0; i < slots.size(); ++i) t[i] = p->blk_epoch[slots[i] / kBlockTok];
+    return t;
+}
+std::vector<uint32_t> block_tags(halo_pool p, const std::vector<int32_t> &blocks) {
+    std::vector<uint32_t> t(blocks.size());
+    for (size_t i = 0; i < blocks.size(); ++i) t[i] = p->blk_epoch[blocks[i]];
+    return t;
 }
 
 // Return blocks that were never handed to the device (error paths).
@@ -1287,7 +1301,8 @@ halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
     auto *p = new halo_pool_s();
     p->cfg = c;
     p->host_only = c.device < 0;
-    p->geom = PoolGeom{c.num_layers, c.num_kv_heads, c.num_q_heads, c.head_dim, c.capacity_blocks};
+    p->geom = PoolGeom{c.num_layers, c.num_kv_heads, c.num_q_heads, c.head_dim, c.capacity_blocks, nullptr};
+    p->blk_epoch.assign(c.capacity_blocks, 0);
     p->free_list.reserve(c.capacity_blocks);
     for (int64_t b = c.capacity_blocks - 1; b >= 0; --b) p->free_list.push_back((int32_t)b);
     if (!p->host_only) {
@@ -1328,7 +1343,14 @@ halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
             p->own_storage = true;
         }
         halo_status st = HALO_OK;
-        if (cudaMemset(p->k, 0, bytes) != cudaSuccess || cudaMemset(p->v, 0, bytes) != cudaSuccess)
+        const size_t vbytes = (size_t)c.num_layers * c.capacity_blocks * sizeof(uint64_t);
+        if (cudaMalloc(&p->geom.vmax, vbytes) != cudaSuccess) {
+            cudaGetLastError();
+            p->geom.vmax = nullptr;
+            st = fail(HALO_ENOMEM, "cudaMalloc of the V table (%zu bytes) failed", vbytes);
+        }
+        if (st == HALO_OK && (cudaMemset(p->k, 0, bytes) != cudaSuccess || cudaMemset(p->v, 0, bytes) != cudaSuccess ||
+                              cudaMemset(p->geom.vmax, 0, vbytes) != cudaSuccess))
             st = fail(HALO_ECUDA, "cudaMemset of the pool failed");
         if (st == HALO_OK) st = make_tmap(p, p->k, &p->tmap_k, 1);
         if (st == HALO_OK) st = make_tmap(p, p->v, &p->tmap_v, 1);
@@ -1339,6 +1361,7 @@ halo_status halo_pool_create(const halo_pool_config *cfg, halo_pool *out) {
                 cudaFree(p->k);
                 cudaFree(p->v);
             }
+            if (p->geom.vmax) cudaFree(p->geom.vmax);
             delete p;
             return st;
         }
@@ -1372,6 +1395,7 @@ halo_status halo_pool_destroy(halo_pool p) {
             cudaFree(p->k);
             cudaFree(p->v);
         }
+        if (p->geom.vmax) cudaFree(p->geom.vmax);
     }
     delete p;
     return HALO_OK;
@@ -1414,13 +1438,17 @@ halo_status halo_prefix_register(halo_pool p, int64_t parent, int32_t ntok, cons
     if (!p->host_only) {
         const size_t bytes = (size_t)p->cfg.num_layers * ntok * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
         std::vector<int32_t> slots = token_slots(blocks, nblk * kBlockTok);
+        std::vector<uint32_t> tags = slot_tags(p, slots);
+        slots.insert(slots.end(), tags.begin(), tags.end());  // one upload: slots | tags
         Scratch ss, sk, sv;
         const void *dk = nullptr, *dvp = nullptr;
         st = upload(slots.data(), slots.size() * 4, s, ss);
         if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
         if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
         if (st == HALO_OK) {
-            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, ntok, (const int32_t *)ss.ptr, ntok,
+            const int32_t *ds = (const int32_t *)ss.ptr;
+            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, ntok, ds,
+                                              (const uint32_t *)(ds + nblk * kBlockTok), ntok,
                                               nblk * kBlockTok - ntok, 0, p->cfg.num_layers, p->num_sms, s);
             if (e != cudaSuccess) st = fail(HALO_ECUDA, "scatter launch: %s", cudaGetErrorString(e));
         }
@@ -1611,12 +1639,17 @@ halo_status halo_suffix_append(halo_pool p, int32_t nreq, const int64_t *reqs, c
         const size_t bytes = (size_t)p->cfg.num_layers * w.total * p->cfg.num_kv_heads * p->cfg.head_dim * 2;
         Scratch ss, sk, sv;
         const void *dk = nullptr, *dvp = nullptr;
-        st = upload(w.slots.data(), w.slots.size() * 4, s, ss);
+        std::vector<int32_t> st_buf = w.slots;
+        std::vector<uint32_t> tags = slot_tags(p, w.slots);
+        st_buf.insert(st_buf.end(), tags.begin(), tags.end());  // slots | tags
+        st = upload(st_buf.data(), st_buf.size() * 4, s, ss);
         if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
         if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
         if (st == HALO_OK) {
-            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, w.total, (const int32_t *)ss.ptr,
-                                              w.total, 0, 0, p->cfg.num_layers, p->num_sms, s);
+            const int32_t *ds = (const int32_t *)ss.ptr;
+            cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dvp, w.total, ds,
+                                              (const uint32_t *)(ds + w.total), w.total, 0, 0,
+                                              p->cfg.num_layers, p->num_sms, s);
             if (e != cudaSuccess) st = fail(HALO_ECUDA, "scatter launch: %s", cudaGetErrorString(e));
         }
         if (st != HALO_OK) {
@@ -1907,13 +1940,16 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
     if (q_host && (st = grow(&pl->q_stage, &pl->q_stage_cap, q_layer * L * 2)) != HALO_OK) return st;
     if (o_host && (st = grow((void **)&pl->o_stage, &pl->o_stage_cap, q_layer * L * 4)) != HALO_OK) return st;
     if (l_host && (st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * L * 4)) != HALO_OK) return st;
-    if ((st = grow((void **)&pl->slot_stage, &pl->slot_stage_cap, w.slots.size() * 4)) != HALO_OK) return st;
+    if ((st = grow((void **)&pl->slot_stage, &pl->slot_stage_cap, w.slots.size() * 8)) != HALO_OK) return st;
     {
-        void *hs = pl->pin_slots.acquire(w.slots.size() * 4);
+        void *hs = pl->pin_slots.acquire(w.slots.size() * 8);  // slots | V-table tags
         if (!hs) return fail(HALO_ENOMEM, "pinned slot staging");
         memcpy(hs, w.slots.data(), w.slots.size() * 4);
-        HALO_CUDA(pl->pin_slots.commit(pl->slot_stage, w.slots.size() * 4, s));
+        uint32_t *ht = static_cast<uint32_t *>(hs) + w.slots.size();
+        for (size_t i = 0; i < w.slots.size(); ++i) ht[i] = p->blk_epoch[w.slots[i] / kBlockTok];
+        HALO_CUDA(pl->pin_slots.commit(pl->slot_stage, w.slots.size() * 8, s));
     }
+    const uint32_t *slot_tags_dev = reinterpret_cast<const uint32_t *>(pl->slot_stage + w.slots.size());
     // 3. pipeline: H2D (k, v, q) on the h2d stream in chunks of kH2DLayers layers, all issued
     //    up front | K5 append + K1 + K2/K3 of layer l on `stream` (waits for its chunk) | D2H
     //    (out, lse) on the d2h stream in chunks of kD2HLayers layers.  Chunk sizes measured on
@@ -1946,15 +1982,15 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
     float *dout = o_host ? pl->o_stage : out;
     float *dlse = l_host ? pl->l_stage : lse;
     if (!kv_host) {  // device-resident new K/V: one K5 launch appends every layer
-        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dv, nreq, pl->slot_stage, nreq, 0, 0, L,
-                                          p->num_sms, s);
+        cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk, dv, nreq, pl->slot_stage, slot_tags_dev,
+                                          nreq, 0, 0, L, p->num_sms, s);
         if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
     }
     for (int l = 0; l < L; ++l) {
         if (l % kH2DLayers == 0) HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_in[l], 0));
         if (kv_host) {  // host K/V: append layer l once its copy has landed
             cudaError_t e = launch_kv_scatter(p->geom, p->k, p->v, dk + kv_layer * l, dv + kv_layer * l, nreq,
-                                              pl->slot_stage, nreq, 0, l, l + 1, p->num_sms, s);
+                                              pl->slot_stage, slot_tags_dev, nreq, 0, l, l + 1, p->num_sms, s);
             if (e != cudaSuccess) return fail(HALO_ECUDA, "append launch: %s", cudaGetErrorString(e));
         }
         st = run_layer(pl, l, dq + q_layer * l, dout + q_layer * l, dlse ? dlse + rows * l : nullptr, scale, s);
@@ -2177,6 +2213,7 @@ halo_status halo_migrate_exchange(halo_pool p, int32_t nsend, const halo_migrate
         x.blocks = blocks;
         x.dev_off = (int64_t)lists.size();
         lists.insert(lists.end(), blocks->begin(), blocks->end());
+        for (int32_t b : *blocks) lists.push_back((int32_t)p->blk_epoch[b]);  // V-table tags
         x.slice = (size_t)(std::min(R, x.items) * item_bytes);
         x.buf_off = per_parity;
         per_parity += x.slice;
@@ -2206,7 +2243,8 @@ halo_status halo_migrate_exchange(halo_pool p, int32_t nsend, const halo_migrate
             if (x.send || c >= x.nchunks) continue;
             const int64_t i0 = c * R, i1 = std::min(x.items, i0 + R);
             cudaError_t e = launch_kv_runs(p->geom, p->k, p->v, base + b * per_parity + x.buf_off,
-                                           dlist + x.dev_off, (int32_t)x.nblk, i0, i1, true, ctas, s);
+                                           dlist + x.dev_off, (const uint32_t *)(dlist + x.dev_off + x.nblk),
+                                           (int32_t)x.nblk, i0, i1, true, ctas, s);
             if (e != cudaSuccess) return fail(HALO_ECUDA, "unpack launch: %s", cudaGetErrorString(e));
         }
         return HALO_OK;
@@ -2219,7 +2257,7 @@ halo_status halo_migrate_exchange(halo_pool p, int32_t nsend, const halo_migrate
             if (!x.send || c >= x.nchunks) continue;
             const int64_t i0 = c * R, i1 = std::min(x.items, i0 + R);
             cudaError_t e = launch_kv_runs(p->geom, p->k, p->v, base + b * per_parity + x.buf_off,
-                                           dlist + x.dev_off, (int32_t)x.nblk, i0, i1, false, ctas, s);
+                                           dlist + x.dev_off, nullptr, (int32_t)x.nblk, i0, i1, false, ctas, s);
             if (e != cudaSuccess) return fail(HALO_ECUDA, "pack launch: %s", cudaGetErrorString(e));
         }
         HALO_CUDA(cudaEventRecord(ev_packed[b], s));
@@ -2308,15 +2346,17 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
     halo_status st = alloc_blocks(dst, nblk, blocks);
     if (st != HALO_OK) return st;
     // whole-block pool-to-pool copy: a (layer, block) of all heads is contiguous on both sides
-    std::vector<int32_t> pairs(2 * nblk);
+    std::vector<int32_t> pairs(3 * nblk);  // pairs | destination tags
     for (int64_t b = 0; b < nblk; ++b) {
         pairs[2 * b] = it->second.blocks[b];
         pairs[2 * b + 1] = blocks[b];
+        pairs[2 * nblk + b] = (int32_t)dst->blk_epoch[blocks[b]];
     }
     Scratch sp;
     if ((st = upload(pairs.data(), pairs.size() * 4, s, sp)) == HALO_OK) {
-        cudaError_t e = launch_kv_copy_blocks(src->geom, src->k, src->v, dst->geom, dst->k, dst->v,
-                                              (const int32_t *)sp.ptr, (int32_t)nblk, 0,
+        const int32_t *dp = (const int32_t *)sp.ptr;
+        cudaError_t e = launch_kv_copy_blocks(src->geom, src->k, src->v, dst->geom, dst->k, dst->v, dp,
+                                              (const uint32_t *)(dp + 2 * nblk), (int32_t)nblk, 0,
                                               src->cfg.num_layers, src->num_sms, s);
         if (e != cudaSuccess) st = fail(HALO_ECUDA, "clone launch: %s", cudaGetErrorString(e));
     }
@@ -2400,7 +2440,17 @@ halo_status halo_prefix_fetch(halo_pool p, int64_t node, void *stream) {
     if (st != HALO_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     if (!p->host_only) {
-        st = copy_node_blocks(p, db, n.host_blocks, false, s);
+        std::vector<int32_t> bt(db);  // blocks | tags: the V-table entries are recomputed
+        for (int32_t b : db) bt.push_back((int32_t)p->blk_epoch[b]);
+        Scratch sb;
+        st = upload(bt.data(), bt.size() * 4, s, sb);
+        if (st == HALO_OK) st = copy_node_blocks(p, db, n.host_blocks, false, s);
+        if (st == HALO_OK) {
+            const int32_t *d = (const int32_t *)sb.ptr;
+            cudaError_t e = launch_kv_vmax(p->geom, p->v, d, (const uint32_t *)(d + db.size()), (int32_t)db.size(),
+                                           p->num_sms, s);
+            if (e != cudaSuccess) st = fail(HALO_ECUDA, "V-table launch: %s", cudaGetErrorString(e));
+        }
         if (st != HALO_OK) {
             unalloc_blocks(p, db, 0);
             return st;

@@ -105,6 +105,8 @@ struct halo_pool_s {
     void *k = nullptr, *v = nullptr;
     bool own_storage = false;
     std::vector<int32_t> free_list;  // stack: back() is the next block handed out
+    std::vector<uint32_t> blk_epoch; // allocation epoch of each block (V-table tag)
+    uint32_t epoch = 0;              // incremented per allocation
     std::vector<halo::PendingFree> pending;
     std::vector<cudaEvent_t> event_cache;
     std::vector<halo::StreamFence> streams;  // streams that enqueued work on this pool

@@ -51,6 +51,18 @@ class Workload:
     # of every root node gets the key K0 * e_0 and every query gets +SINK_QB on dim 0, so its
     # scaled score is sink * (1 + z * alpha / SINK_QB) with z ~ N(0,1): +sink on average.
     sink: float = 0.0
+    # value distribution of every tensor (synth.gen: "grid" = round-1 multiples of 1/32,
+    # "normal" = bf16(N(0,1)) with a full mantissa)
+    dist: str = "grid"
+    # outlier channels: K (nodes, suffixes, new tokens) dims in `k_outlier_dims` x 2^k_outlier_log2
+    k_outlier_dims: tuple = ()
+    k_outlier_log2: int = 6
+    # V magnitude per prefix node: node ident -> p, its V x 2^p (exact); requests whose leaf
+    # is that node get the same factor on their suffix and appended V (the whole context of
+    # such a request is scaled, so its exact output scales by 2^p: o(aV) = a o(V))
+    v_scale_log2: dict = field(default_factory=dict)
+    # within a node: node ident -> (tok0, p): its tokens [tok0, ntok) get an extra V x 2^p
+    v_token_scale_log2: dict = field(default_factory=dict)
     notes: dict = field(default_factory=dict)
 
     # ---- structure -------------------------------------------------------------------
@@ -91,9 +103,42 @@ class Workload:
 
     SINK_QB = 4.0  # query bias on dim 0 of the sink variant
 
+    # ---- value shaping (exact: powers of two) -----------------------------------------
+    def _k_out(self, k):
+        if self.k_outlier_dims:
+            k = k.clone()
+            idx = list(self.k_outlier_dims)
+            k[..., idx] = (k[..., idx].float() * 2.0 ** self.k_outlier_log2).to(torch.bfloat16)
+        return k
+
+    def _v_scale(self, v, leaf_of_rows=None, node=None):
+        """Scale V by 2^p: of node `node`, or per row (dim -3) by the scale of each row's leaf."""
+        if not self.v_scale_log2:
+            return v
+        if node is not None:
+            p = self.v_scale_log2.get(node, 0)
+            return v if p == 0 else (v.float() * 2.0 ** p).to(torch.bfloat16)
+        f = torch.tensor([2.0 ** self.v_scale_log2.get(lf, 0) for lf in leaf_of_rows],
+                         dtype=torch.float32, device=v.device)
+        return (v.float() * f[:, None, None]).to(torch.bfloat16)
+
+    def _row_leaves(self, request=None):
+        """Leaf of every initial-suffix token row (or of request `request`'s rows)."""
+        if request is not None:
+            return [self.requests[request].leaf] * self.requests[request].suffix
+        return [r.leaf for r in self.requests for _ in range(r.suffix)]
+
     def node_kv(self, n: int, device="cpu", layer=None):
         nt = self.node(n).ntok
         k, v = self._pair("node_k", "node_v", n, nt, self.hkv, device, layer)
+        k, v = self._k_out(k), self._v_scale(v, node=n)
+        if n in self.v_token_scale_log2:
+            t0, p = self.v_token_scale_log2[n]
+            v = v.clone()
+            if layer is None:
+                v[:, t0:] = (v[:, t0:].float() * 2.0 ** p).to(torch.bfloat16)
+            else:
+                v[t0:] = (v[t0:].float() * 2.0 ** p).to(torch.bfloat16)
         if self.sink > 0 and self.node(n).parent < 0:
             # K0 = sink * sqrt(d) / SINK_QB on dim 0, zero elsewhere (exact in bf16 after rounding)
             k0 = torch.zeros(self.hkv, self.d, dtype=torch.float32)
@@ -110,13 +155,19 @@ class Workload:
         tot = int(self.suffix_offsets[-1])
         row = self.hkv * self.d
         if request is None:
-            return self._pair("suf_k", "suf_v", 0, tot, self.hkv, device, layer)
+            k, v = self._pair("suf_k", "suf_v", 0, tot, self.hkv, device, layer)
+            if self.v_scale_log2:
+                lv = self._row_leaves()
+                v = self._v_scale(v, lv) if layer is not None else \
+                    torch.stack([self._v_scale(v[i], lv) for i in range(v.shape[0])])
+            return self._k_out(k), v
         s0, s1 = int(self.suffix_offsets[request]), int(self.suffix_offsets[request + 1])
         assert layer is not None
         off = (layer * tot + s0) * row
         shape = (s1 - s0, self.hkv, self.d)
-        return (bf16_tensor(self._key("suf_k", 0), shape, device, off),
-                bf16_tensor(self._key("suf_v", 0), shape, device, off))
+        k = bf16_tensor(self._key("suf_k", 0), shape, device, off, dist=self.dist)
+        v = bf16_tensor(self._key("suf_v", 0), shape, device, off, dist=self.dist)
+        return self._k_out(k), self._v_scale(v, self._row_leaves(request))
 
     def q(self, step: int, device="cpu", layer=None, request=None):
         """Decode queries of step `step`: [L][R][Hq][d] (or a slice)."""
@@ -127,8 +178,16 @@ class Workload:
 
     def new_kv(self, step: int, device="cpu", layer=None, request=None):
         """K/V of the token appended at step `step`: [L][R][Hkv][d] (or a slice)."""
-        return (self._rows("new_k", step, self.hkv, device, layer, request),
-                self._rows("new_v", step, self.hkv, device, layer, request))
+        k = self._k_out(self._rows("new_k", step, self.hkv, device, layer, request))
+        v = self._rows("new_v", step, self.hkv, device, layer, request)
+        if self.v_scale_log2:
+            if request is not None:
+                v = self._v_scale(v[None], [self.requests[request].leaf])[0]
+            else:
+                lv = [r.leaf for r in self.requests]
+                v = self._v_scale(v, lv) if layer is not None else \
+                    torch.stack([self._v_scale(v[i], lv) for i in range(v.shape[0])])
+        return k, v
 
     def _pair(self, kk, kv, ident, ntok, heads, device, layer):
         row = heads * self.d
@@ -136,8 +195,8 @@ class Workload:
             shape, off = (self.layers, ntok, heads, self.d), 0
         else:
             shape, off = (ntok, heads, self.d), layer * ntok * row
-        return (bf16_tensor(self._key(kk, ident), shape, device, off),
-                bf16_tensor(self._key(kv, ident), shape, device, off))
+        return (bf16_tensor(self._key(kk, ident), shape, device, off, dist=self.dist),
+                bf16_tensor(self._key(kv, ident), shape, device, off, dist=self.dist))
 
     def _rows(self, kind, ident, heads, device, layer, request, alpha=1.0):
         R = self.nreq
@@ -145,12 +204,12 @@ class Workload:
         if layer is None:
             assert request is None
             return bf16_tensor(self._key(kind, ident), (self.layers, R, heads, self.d), device,
-                               0, alpha)
+                               0, alpha, dist=self.dist)
         if request is None:
             return bf16_tensor(self._key(kind, ident), (R, heads, self.d), device,
-                               layer * R * row, alpha)
+                               layer * R * row, alpha, dist=self.dist)
         return bf16_tensor(self._key(kind, ident), (heads, self.d), device,
-                           (layer * R + request) * row, alpha)
+                           (layer * R + request) * row, alpha, dist=self.dist)
 
 
 # ---------------------------------------------------------------------------------------
@@ -216,7 +275,21 @@ def ragged_suffix(seed=5, layers=2, nreq=96, prefix=1024, lo=128, hi=1024, hq=32
     return Workload("ragged_suffix", layers, hq, hkv, d, nodes, reqs, seed, **kw)
 
 
+def scaled(seed=6, layers=2, hq=8, hkv=2, d=128, dist="normal", **kw):
+    """V-range stress (K1 converts V to fp16 for the P.V MMA): three roots -- unit-scale V
+    whose tokens 600.. are x 2^20 (the fp16 scale must grow inside a tile), V x 2^17 (|V| up to ~8e5, beyond fp16's 65504) and V x 2^-22 (|V| <= ~1.4e-6, below
+    fp16's normal range) -- plus a unit-scale child under the huge root, requests on every
+    node with ragged suffixes scaled like their leaf; full-mantissa normal values."""
+    nodes = [NodeSpec(0, -1, 1000), NodeSpec(1, -1, 777), NodeSpec(2, -1, 640),
+             NodeSpec(3, 1, 300)]
+    reqs = [RequestSpec(i, i % 4, 20 + 37 * (i % 5)) for i in range(64)]
+    kw.setdefault("v_scale_log2", {1: 17, 2: -22})
+    kw.setdefault("v_token_scale_log2", {0: (600, 20)})  # V grows x 2^20 mid-node
+    return Workload("scaled", layers, hq, hkv, d, nodes, reqs, seed, dist=dist, **kw)
+
+
 CONFIGS = {
+    "scaled": scaled,
     "toy": toy,
     "fanout": fanout,
     "tree": tree,

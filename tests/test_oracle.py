@@ -310,3 +310,47 @@ def test_sink_variant_inputs():
         assert abs(s0.mean().item() - 8.0) < 0.5 and abs(s5.mean().item()) < 0.5
     assert float(k[0, 0, 0, 1]) == 0.0
     assert abs(float(k[0, 0, 0, 0]) - 8.0 * wl.d ** 0.5 / wl.SINK_QB) < 0.1
+
+
+def test_normal_generator_full_mantissa_and_moments():
+    """dist="normal" (bf16(N(0,1))): unit moments, tails bounded by the
+    Irwin-Hall(12) support, values NOT on the 1/32 grid (full 8-bit significands), slices
+    consistent, CPU generation deterministic."""
+    key = TensorKey(9, "node_v", 1)
+    a = bf16_tensor(key, (1 << 18,), dist="normal")
+    assert torch.equal(a[1000:], bf16_tensor(key, ((1 << 18) - 1000,), offset=1000, dist="normal"))
+    assert torch.equal(a, bf16_tensor(key, (1 << 18,), dist="normal"))
+    x = a.double()
+    assert abs(float(x.mean())) < 0.01 and abs(float(x.std()) - 1.0) < 0.01
+    assert float(x.abs().max()) <= 1530 / 256
+    assert float((x * 32 != (x * 32).round()).double().mean()) > 0.5
+    # excess kurtosis of Irwin-Hall(12) is -0.1 (a Gaussian's is 0)
+    k = float(((x - x.mean()) ** 4).mean() / x.var() ** 2) - 3
+    assert -0.2 < k < 0.05
+
+
+def test_scaled_workload_inputs_are_exact_power_of_two_scalings():
+    """The V-range stress workload scales V by exact powers of two (node, token ramp, and the
+    leaf's factor on its requests' suffix / new tokens); K and q are untouched; the per-layer
+    and per-request slices equal the full tensors."""
+    wl = make_config("scaled")
+    base = make_config("scaled", v_scale_log2={}, v_token_scale_log2={})
+    for n, p in [(0, 0), (1, 17), (2, -22), (3, 0)]:
+        k, v = wl.node_kv(n, "cpu")
+        kb, vb = base.node_kv(n, "cpu")
+        assert torch.equal(k, kb)
+        f = torch.full((v.shape[1],), 2.0 ** p, dtype=torch.float64)
+        if n == 0:
+            f[600:] *= 2.0 ** 20
+        assert torch.equal(v.double(), vb.double() * f[None, :, None, None])
+        assert torch.equal(wl.node_kv(n, "cpu", 1)[1], v[1])
+    sk, sv = wl.suffix_kv("cpu")
+    _, svb = base.suffix_kv("cpu")
+    for r in range(0, wl.nreq, 7):
+        s0, s1 = int(wl.suffix_offsets[r]), int(wl.suffix_offsets[r + 1])
+        p = wl.v_scale_log2.get(wl.requests[r].leaf, 0)
+        assert torch.equal(sv[:, s0:s1].double(), svb[:, s0:s1].double() * 2.0 ** p)
+        assert torch.equal(wl.suffix_kv("cpu", 1, request=r)[1], sv[1, s0:s1])
+        nv = wl.new_kv(0, "cpu", 1, request=r)[1]
+        assert torch.equal(nv.double(), base.new_kv(0, "cpu", 1, request=r)[1].double() * 2.0 ** p)
+        assert torch.equal(wl.new_kv(0, "cpu")[1][1, r], nv)

@@ -28,7 +28,14 @@
  * last error on the calling thread is returned by halo_last_error().
  *
  * Threading: a pool (and its plans) is externally synchronised -- one host thread at a
- * time.  All device work is stream-ordered on the caller's stream.
+ * time.  All device work is stream-ordered on the caller's stream.  Blocks given back
+ * (request close, truncate, prefix release, MOVE, offload) return to the free list once the
+ * work enqueued so far on every stream that used the pool (the 16 most recent; an older one is
+ * synchronised before it is forgotten) has passed.
+ *
+ * Plans: a plan records block ids.  Any call that gives blocks back or moves a node (the list
+ * above, fetch) makes every plan built before it stale: halo_decode_run then returns
+ * HALO_EBUSY; re-plan (halo_decode_plan with the plan as *inout).
  *
  * Ids: node and request ids are int64, unique and never reused within a pool.
  */
@@ -144,6 +151,7 @@ halo_status halo_suffix_truncate(halo_pool pool, int32_t nreq, const int64_t *re
                                  const int32_t *ntok);
 
 /* ------------------------------------------------------------------ decode step */
+/* A zero-initialised struct (or NULL) selects every default. */
 typedef struct {
     int32_t min_tensor_rows; /* a prefix node runs on the tcgen05 prefix kernel (K1) iff
                                 (#requests under it) * g >= this; others are folded into
@@ -152,6 +160,13 @@ typedef struct {
                                 (tests); 0: the plan chooses (fills the 148 SMs).      */
     int32_t max_splits;      /* cap on splits per node; <= 0: default 16                */
     int32_t k2_chunk_blocks; /* K2 work-queue chunk in 16-token blocks; <= 0: plan chooses */
+    int32_t k2_shape;        /* K2 launch shape: 0 = plan chooses, 1 = wide (12 warps x 2
+                                ring stages per SM), 2 = narrow (7 warps x 4 stages)    */
+    int32_t k2_sms;          /* > 0: K2's schedule and grid use this many SMs; 0 = all    */
+    float k1_sm_frac;        /* single-wave K1 beside a dominant K2 may take this fraction
+                                of the SMs (K2); 0 = default 0.65, < 0 = off   */
+    float k2_early_weight;   /* work weight of K2 warps that start beside K1 (on SMs K1
+                                leaves idle); 0 = default (1.2 when the K1 rule applies) */
 } halo_plan_options;
 
 /* Build (or rebuild in place, when *inout != NULL) the plan of one decode step for the

@@ -156,11 +156,17 @@ void note_stream(halo_pool p, cudaStream_t s) {
             f.last_use = p->use_clock;
             return;
         }
-    if (p->streams.size() >= 8) {
+    if (p->streams.size() >= 16) {
+        // forget the least recently used stream -- after its enqueued work has finished, so a
+        // later release (which fences only the listed streams) cannot free blocks it still reads
         auto it = std::min_element(p->streams.begin(), p->streams.end(),
                                    [](const StreamFence &a, const StreamFence &b) {
                                        return a.last_use < b.last_use;
                                    });
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(it->stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone)
+            cudaStreamSynchronize(it->stream);
+        cudaGetLastError();
         *it = StreamFence{s, p->use_clock};
     } else {
         p->streams.push_back(StreamFence{s, p->use_clock});
@@ -226,6 +232,7 @@ void unalloc_blocks(halo_pool p, const std::vector<int32_t> &blocks, size_t from
 // pool has passed (events recorded now).
 void release_blocks(halo_pool p, std::vector<int32_t> &&blocks) {
     if (blocks.empty()) return;
+    p->layout_gen++;  // plans built before this may read these blocks: they are stale now
     if (p->host_only) {
         for (auto it = blocks.rbegin(); it != blocks.rend(); ++it) p->free_list.push_back(*it);
         return;
@@ -386,74 +393,15 @@ int choose_chunk(const std::vector<PNode> &ns, int g, int hkv, int nsm, int max_
     return best_c;
 }
 
-// Experiment hook (HALO_K2_SMS=n): K2's schedule and grid use n SMs instead of all.
-int k2_sms(halo_pool p) {
-    static const int n = [] {
-        const char *e = getenv("HALO_K2_SMS");
-        return e ? atoi(e) : 0;
-    }();
-    return (n > 0 && n < p->num_sms) ? n : p->num_sms;
+// Plan options (halo_plan_options) with their defaults applied.
+int k2_sms(halo_plan pl) {
+    const int n = pl->opt.k2_sms, all = pl->pool->num_sms;
+    return (n > 0 && n < all) ? n : all;
 }
-
-// Experiment hook (HALO_K2_EARLY_W=x): weight of the K2 warps whose CTAs start on SMs that K1
-// leaves idle (blockIdx < num_sms - K1 CTAs) relative to those that enter as K1 retires.
-double k2_early_weight_env() {
-    static const double w = [] {
-        const char *e = getenv("HALO_K2_EARLY_W");
-        return e ? atof(e) : 1.2;
-    }();
-    return w;
-}
-
-// Experiment hook (HALO_K1_SM_FRAC=x, 0 disables): the fraction of the SMs a single-wave K1
-// may occupy when K2 dominates the layer (section 7 of the planner).
-double k1_sm_frac() {
-    static const double f = [] {
-        const char *e = getenv("HALO_K1_SM_FRAC");
-        return e ? atof(e) : 0.65;
-    }();
-    return f;
-}
-
-// Experiment hook (HALO_K2_SHARED_NORMAL=0): stream folded prefix-node blocks with
-// evict_first like the private suffix blocks.
-bool k2_shared_normal() {
-    static const bool v = [] {
-        const char *e = getenv("HALO_K2_SHARED_NORMAL");
-        return e ? atoi(e) != 0 : true;
-    }();
-    return v;
-}
-
-// Experiment hook (HALO_K2_FORCE_WIDE=1): always use K2's wide launch shape.
-bool force_wide() {
-    static const bool f = [] {
-        const char *e = getenv("HALO_K2_FORCE_WIDE");
-        return e && atoi(e) != 0;
-    }();
-    return f;
-}
-
-// Experiment hook (HALO_K2_AUTO_NARROW=1): let the planner pick the narrow shape whenever
-// whole units balance on it.  By default only for short units (< 8 blocks on average):
-// since the L2 evict_first policy on the suffix stream (session 4) the wide shape wins at
-// C1 (17 blocks per unit: K2 0.81 vs 0.77 of HBM), while 1-2-block units (16-token
-// suffixes) stay 20% faster on the narrow one (K2).
-bool auto_narrow() {
-    static const bool f = [] {
-        const char *e = getenv("HALO_K2_AUTO_NARROW");
-        return e && atoi(e) != 0;
-    }();
-    return f;
-}
-
-// Test hook (HALO_K2_FORCE_NARROW=1): always use K2's narrow launch shape.
-bool force_narrow() {
-    static const bool f = [] {
-        const char *e = getenv("HALO_K2_FORCE_NARROW");
-        return e && atoi(e) != 0;
-    }();
-    return f;
+double k2_early_weight(halo_plan pl) { return pl->opt.k2_early_weight > 0 ? pl->opt.k2_early_weight : 1.2; }
+double k1_sm_frac(halo_plan pl) {
+    const float f = pl->opt.k1_sm_frac;
+    return f < 0 ? 0.0 : f == 0 ? 0.65 : (double)f;
 }
 
 // `virt` (prefill): the plan's rows are these virtual requests -- one per new prompt token,
@@ -599,7 +547,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         // tools/k2_early_sweep3.sh: ratios 2.5-10 gain 3-8%, ratios ~2.1 lose 4-11%).
         // (C1: 4 -> 3 splits, 128 -> 96 K1 CTAs, 3.59 -> 3.71 M queries/s; K2.)
         pl->k2_early = false;
-        if (k1_sm_frac() > 0 && pl->opt.max_splits <= 0) {
+        if (k1_sm_frac(pl) > 0 && pl->opt.max_splits <= 0) {
             auto tiles_for = [&](int64_t Cc, int64_t &max_ch) {
                 int64_t T = 0;
                 max_ch = 0;
@@ -618,7 +566,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             const int64_t T0 = tiles_for(C, mc);
             double k2_bytes_est = 0;
             for (int i = 0; i < nreq; ++i) k2_bytes_est += (double)R[i]->blocks.size() * kBlockTok * hkv * D * 4;
-            const double cap = k1_sm_frac() * p->num_sms;
+            const double cap = k1_sm_frac(pl) * p->num_sms;
             if (T0 > 0 && T0 <= p->num_sms && (double)T0 > cap) {
                 for (int64_t Cc = C + kK1Tok; Cc <= kK1MaxTileTok; Cc += kK1Tok) {
                     const int64_t T1 = tiles_for(Cc, mc);
@@ -818,7 +766,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     // over the warps.  Chunks are contiguous item ranges of about equal weight.
     {
         const int U = nreq * hkv;
-        const int64_t Ww = (int64_t)k2_sms(p) * kK2WarpsWide, Wn = (int64_t)k2_sms(p) * kK2WarpsNarrow;
+        const int64_t Ww = (int64_t)k2_sms(pl) * kK2WarpsWide, Wn = (int64_t)k2_sms(pl) * kK2WarpsNarrow;
         pl->k2_warps = kK2WarpsWide;
         pl->unit_boff.assign(U + 1, 0);
         for (int u = 0; u < U; ++u) {
@@ -849,9 +797,8 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         // first num_sms - (K1 CTAs) land on SMs K1 leaves idle and stream while K1 runs; the
         // rest enter as K1's CTAs retire.  Warps of the early CTAs get `ew` times the share.
         const int64_t k1c = (int64_t)pl->tiles.size();
-        const int64_t early_ctas = (k1c > 0 && k1c < k2_sms(p)) ? k2_sms(p) - k1c : 0;
-        const double ew = early_ctas > 0 && (pl->k2_early || getenv("HALO_K2_EARLY_W")) && k2_early_weight_env() > 0
-                              ? k2_early_weight_env() : 1.0;
+        const int64_t early_ctas = (k1c > 0 && k1c < k2_sms(pl)) ? k2_sms(pl) - k1c : 0;
+        const double ew = early_ctas > 0 && (pl->k2_early || pl->opt.k2_early_weight > 0) ? k2_early_weight(pl) : 1.0;
         auto target = [&](int64_t w, int64_t nw, int wpc) -> int64_t {  // item position of cut w
             if (ew == 1.0) return w * Itot / nw;
             const int64_t ne = std::min<int64_t>(nw, early_ctas * wpc);
@@ -890,12 +837,12 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             cuts.assign(1, 0);
             for (int64_t x = pl->opt.k2_chunk_blocks; x < Itot; x += pl->opt.k2_chunk_blocks) push_cut(cuts, x);
             cuts.push_back(Itot);
-        } else if (force_narrow()) {  // test hook
+        } else if (pl->opt.k2_shape == 2) {  // forced narrow shape
             pl->k2_warps = kK2WarpsNarrow;
             cuts = equal_cuts(Wn, kK2WarpsNarrow);
-        } else if (force_wide()) {  // experiment hook
+        } else if (pl->opt.k2_shape == 1) {  // forced wide shape
             cuts = equal_cuts(Ww, kK2WarpsWide);
-        } else if ((auto_narrow() || Btot < 8 * (int64_t)U) && U < 2 * Ww &&
+        } else if (Btot < 8 * (int64_t)U && U < 2 * Ww &&
                    (cuts = snapped_cuts(Wn, kK2WarpsNarrow, bal), bal)) {
             // few units per warp (stream-K pieces would dominate) and whole units divide
             // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
@@ -958,7 +905,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
                 // bit 31: a block of a folded prefix node, read by every request under the node:
                 // K2 streams it with the default L2 policy instead of evict_first
                 pl->k2_ent[2 * (size_t)x + 1] = (uint32_t)(req * hkv + head) |
-                                                ((x - b0) < req_fold_blk[req] && k2_shared_normal() ? 0x80000000u : 0u);
+                                                ((x - b0) < req_fold_blk[req] ? 0x80000000u : 0u);
             }
             int32_t *um = &pl->unit_meta[(size_t)uu * 8];
             um[0] = b0; um[1] = b1; um[2] = req; um[3] = head;
@@ -1114,7 +1061,7 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
     dv.seg_o = pl->segbuf;
     dv.seg_ml = pl->segbuf + (size_t)pl->nseg_total * gq * p->cfg.head_dim;
-    dv.nwarps = k2_sms(p) * pl->k2_warps;
+    dv.nwarps = k2_sms(pl) * pl->k2_warps;
     dv.k2_warps = pl->k2_warps;
     dv.ntiles = (int32_t)pl->tiles.size();
     dv.nreq = nreq;
@@ -1127,7 +1074,7 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
                       float scale, cudaStream_t s, int mask = 3) {
     halo_pool p = pl->pool;
     if (pl->layout_gen != p->layout_gen)
-        return fail(HALO_EBUSY, "stale plan: a prefix node was offloaded or fetched since it was built");
+        return fail(HALO_EBUSY, "stale plan: blocks were given back or a node moved since it was built (re-plan)");
     cudaError_t e;
     if (mask & 1) {
         const CUtensorMap *tq = nullptr;
@@ -1907,6 +1854,10 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
         return st;
     }
     halo_plan pl = *inout;
+    const size_t kv_layer = (size_t)nreq * Hkv * D;     // elements of one layer's new K (or V)
+    const size_t q_layer = (size_t)nreq * Hq * D, rows = (size_t)nreq * Hq;
+    const bool kv_host = !is_device_ptr(k_new) || !is_device_ptr(v_new);
+    const bool q_host = !is_device_ptr(q), o_host = !is_device_ptr(out), l_host = lse && !is_device_ptr(lse);
     // 2. streams, events and staging (grown once)
     auto grow = [&](void **buf, size_t *cap, size_t bytes) -> halo_status {
         if (*cap >= bytes) return HALO_OK;
@@ -1919,35 +1870,41 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
         *cap = bytes;
         return HALO_OK;
     };
-    const size_t kv_layer = (size_t)nreq * Hkv * D;     // elements of one layer's new K (or V)
-    const size_t q_layer = (size_t)nreq * Hq * D, rows = (size_t)nreq * Hq;
-    const bool kv_host = !is_device_ptr(k_new) || !is_device_ptr(v_new);
-    const bool q_host = !is_device_ptr(q), o_host = !is_device_ptr(out), l_host = lse && !is_device_ptr(lse);
-    if (!pl->h2d) {
-        HALO_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking));
-        HALO_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking));
-        HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_step, cudaEventDisableTiming));
-        HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_copied, cudaEventDisableTiming));
-    }
-    while ((int)pl->ev_in.size() < L) {
-        cudaEvent_t a, b;
-        HALO_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
-        HALO_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
-        pl->ev_in.push_back(a);
-        pl->ev_out.push_back(b);
-    }
-    if (kv_host && (st = grow(&pl->kv_stage, &pl->kv_stage_cap, 2 * kv_layer * L * 2)) != HALO_OK) return st;
-    if (q_host && (st = grow(&pl->q_stage, &pl->q_stage_cap, q_layer * L * 2)) != HALO_OK) return st;
-    if (o_host && (st = grow((void **)&pl->o_stage, &pl->o_stage_cap, q_layer * L * 4)) != HALO_OK) return st;
-    if (l_host && (st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * L * 4)) != HALO_OK) return st;
-    if ((st = grow((void **)&pl->slot_stage, &pl->slot_stage_cap, w.slots.size() * 8)) != HALO_OK) return st;
-    {
-        void *hs = pl->pin_slots.acquire(w.slots.size() * 8);  // slots | V-table tags
-        if (!hs) return fail(HALO_ENOMEM, "pinned slot staging");
-        memcpy(hs, w.slots.data(), w.slots.size() * 4);
-        uint32_t *ht = static_cast<uint32_t *>(hs) + w.slots.size();
-        for (size_t i = 0; i < w.slots.size(); ++i) ht[i] = p->blk_epoch[w.slots[i] / kBlockTok];
-        HALO_CUDA(pl->pin_slots.commit(pl->slot_stage, w.slots.size() * 8, s));
+    // everything that can fail before the first launch; on failure the append is rolled back
+    // (the pool is unchanged) and the rebuilt plan is marked stale
+    auto stage = [&]() -> halo_status {
+        if (!pl->h2d) {
+            HALO_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking));
+            HALO_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking));
+            HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_step, cudaEventDisableTiming));
+            HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_copied, cudaEventDisableTiming));
+        }
+        while ((int)pl->ev_in.size() < L) {
+            cudaEvent_t a, b;
+            HALO_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            HALO_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            pl->ev_in.push_back(a);
+            pl->ev_out.push_back(b);
+        }
+        if (kv_host && (st = grow(&pl->kv_stage, &pl->kv_stage_cap, 2 * kv_layer * L * 2)) != HALO_OK) return st;
+        if (q_host && (st = grow(&pl->q_stage, &pl->q_stage_cap, q_layer * L * 2)) != HALO_OK) return st;
+        if (o_host && (st = grow((void **)&pl->o_stage, &pl->o_stage_cap, q_layer * L * 4)) != HALO_OK) return st;
+        if (l_host && (st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * L * 4)) != HALO_OK) return st;
+        if ((st = grow((void **)&pl->slot_stage, &pl->slot_stage_cap, w.slots.size() * 8)) != HALO_OK) return st;
+        {
+            void *hs = pl->pin_slots.acquire(w.slots.size() * 8);  // slots | V-table tags
+            if (!hs) return fail(HALO_ENOMEM, "pinned slot staging");
+            memcpy(hs, w.slots.data(), w.slots.size() * 4);
+            uint32_t *ht = static_cast<uint32_t *>(hs) + w.slots.size();
+            for (size_t i = 0; i < w.slots.size(); ++i) ht[i] = p->blk_epoch[w.slots[i] / kBlockTok];
+            HALO_CUDA(pl->pin_slots.commit(pl->slot_stage, w.slots.size() * 8, s));
+        }
+        return HALO_OK;
+    };
+    if ((st = stage()) != HALO_OK) {
+        rollback();
+        p->layout_gen++;
+        return st;
     }
     const uint32_t *slot_tags_dev = reinterpret_cast<const uint32_t *>(pl->slot_stage + w.slots.size());
     // 3. pipeline: H2D (k, v, q) on the h2d stream in chunks of kH2DLayers layers, all issued

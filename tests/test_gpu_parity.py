@@ -473,28 +473,27 @@ def test_prefill_against_cached_prefixes_matches_oracle(min_rows):
     cleanup(ld, plan)
 
 
-def test_k2_narrow_launch_shape_on_every_head_layout():
+@pytest.mark.parametrize("shape", [1, 2])
+def test_k2_forced_launch_shapes_on_every_head_layout(shape):
     """The planner picks K2's narrow shape (7 warps x 4 stages) only for C1-like batches;
-    force it (HALO_K2_FORCE_NARROW, read once per process: run in a subprocess) on ragged
-    trees, d=64/128 and g=1/2/4/8, stream-K pieces included."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
-        "import test_gpu_parity as t\n"
-        "from synth import make_config\n"
-        "t.halo_build.build(); t.halo.load_library(); t.torch.cuda.set_device(0)\n"
-        "t.check(make_config('ragged'), t.opts(min_rows=16))\n"
-        "t.check(make_config('ragged_suffix', layers=1, nreq=40, prefix=300, lo=1, hi=300))\n"
-        "t.check(make_config('fanout', layers=1, nreq=40, prefix=260, suffix=9, hq=16, hkv=2))\n"
-        "t.check(make_config('fanout', layers=1, nreq=70, prefix=333, suffix=17, hq=4, hkv=2, d=64))\n"
-        "t.check(make_config('fanout', layers=1, nreq=130, prefix=260, suffix=9, hq=4, hkv=4), t.opts(min_rows=1))\n"
-        "print('narrow ok')\n") % (os.path.dirname(os.path.abspath(__file__)),
-                                     os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    env = dict(os.environ, HALO_K2_FORCE_NARROW="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "narrow ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+    force each shape (halo_plan_options.k2_shape) on ragged trees, d=64/128 and g=1/2/4/8,
+    stream-K pieces included."""
+    def o(min_rows=0):
+        return PlanOptions(min_rows, 0, 0, 0, shape)
+    check(make_config("ragged"), o(min_rows=16))
+    check(make_config("ragged_suffix", layers=1, nreq=40, prefix=300, lo=1, hi=300), o())
+    check(make_config("fanout", layers=1, nreq=40, prefix=260, suffix=9, hq=16, hkv=2), o())
+    check(make_config("fanout", layers=1, nreq=70, prefix=333, suffix=17, hq=4, hkv=2, d=64), o())
+    check(make_config("fanout", layers=1, nreq=130, prefix=260, suffix=9, hq=4, hkv=4), o(min_rows=1))
+
+
+def test_plan_options_sm_cap_and_k1_rule():
+    """k2_sms caps K2's grid (a co-scheduled kernel keeps SMs), k1_sm_frac < 0 turns the
+    single-wave K1 rule off, k2_early_weight set explicitly: all still match the oracle."""
+    wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=63)
+    check(wl, PlanOptions(0, 0, 0, 0, 0, 100, 0.0, 0.0))
+    check(wl, PlanOptions(0, 0, 0, 0, 0, 0, -1.0, 0.0))
+    check(wl, PlanOptions(0, 0, 0, 0, 0, 0, 0.0, 1.5))
 
 
 def test_maximum_sizes_long_prefix_and_long_suffix():
@@ -538,4 +537,24 @@ def test_decode_run_is_cuda_graph_capturable():
         torch.cuda.synchronize()
         assert torch.equal(out, eager)
     del g
+    cleanup(ld, plan)
+
+
+def test_plan_is_stale_after_blocks_are_given_back():
+    """A plan records block ids: closing a request (or truncating, releasing, moving) makes
+    plans built before it stale -- halo_decode_run returns EBUSY until it is re-planned."""
+    wl = make_config("fanout", layers=1, nreq=8, prefix=100, suffix=20)
+    ld = load(wl, DEV)
+    append_step(ld, wl, 0, DEV)
+    plan = ld.pool.plan(ld.req_ids[:4])
+    q = wl.q(0, "cuda")[0][:4].contiguous()
+    out = torch.empty((4, wl.hq, wl.d), device="cuda")
+    plan.run(0, q, out)
+    ld.pool.close_request(ld.req_ids[7])
+    with pytest.raises(halo.HaloError) as e:
+        plan.run(0, q, out)
+    assert e.value.name == "HALO_EBUSY"
+    ld.pool.plan(ld.req_ids[:4], reuse=plan)
+    plan.run(0, q, out)
+    torch.cuda.synchronize()
     cleanup(ld, plan)

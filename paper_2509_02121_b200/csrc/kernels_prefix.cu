@@ -424,6 +424,9 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
         int s_cur = 0;  // the tile's V scale exponent: O accumulates P.(V 2^-s)
         for (int n = 0; n < NT; ++n) {
             ptx::mbar_wait(&bar[S_FULL + x], n & 1);
+            // PV_x(n-1) has completed (S_FULL(n) commits after it, in issue order): observe its
+            // phase so every PV_DONE phase is waited on (free; keeps synccheck exact)
+            if (n >= 1) ptx::mbar_wait(&bar[PV_DONE + x], (n - 1) & 1);
             if (threadIdx.x == 0) K1_TRACE(6, n);
             if (threadIdx.x == 128) K1_TRACE(14, n);
             ptx::tc_fence_after();

@@ -46,7 +46,7 @@
 
 #ifdef HALO_K1_TRACE
 // Debug timeline of CTA 0: g_k1_trace[event * 64 + tile] = %globaltimer (ns).
-__device__ unsigned long long *g_k1_trace = nullptr;  // [16][64]
+__device__ unsigned long long *g_k1_trace = nullptr;  // [24][64]
 #define K1_TRACE(ev, n)                                                                 \
     do {                                                                                \
         if (blockIdx.x == 0 && g_k1_trace && (n) < 64) {                                \
@@ -55,11 +55,21 @@ __device__ unsigned long long *g_k1_trace = nullptr;  // [16][64]
             g_k1_trace[(ev) * 64 + (n)] = t_;                                           \
         }                                                                               \
     } while (0)
+// same, recorded only once `dep` has been computed (the timer read takes it as an operand)
+#define K1_TRACE_DEP(ev, n, dep)                                                        \
+    do {                                                                                \
+        if (blockIdx.x == 0 && g_k1_trace && (n) < 64) {                                \
+            unsigned long long t_;                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "f"(dep));          \
+            g_k1_trace[(ev) * 64 + (n)] = t_;                                           \
+        }                                                                               \
+    } while (0)
 extern "C" int halo_debug_k1_trace(void *buf) {
     return (int)cudaMemcpyToSymbol(g_k1_trace, &buf, sizeof(buf));
 }
 #else
 #define K1_TRACE(ev, n) do { } while (0)
+#define K1_TRACE_DEP(ev, n, dep) do { } while (0)
 #endif
 
 namespace halo {
@@ -442,6 +452,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             HALO_TMEM_WAIT_LD_REGS32((sr + 32));
             HALO_TMEM_WAIT_LD_REGS32((sr + 64));
             HALO_TMEM_WAIT_LD_REGS32((sr + 96));
+            if (threadIdx.x == 0) K1_TRACE_DEP(16, n, __uint_as_float(sr[0]));
             if (valid < kK1Tok) {  // only in a node's last n-tile: columns past the end -> -inf
 #pragma unroll
                 for (int i = 0; i < kK1Tok; ++i)
@@ -452,7 +463,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             for (int i = 0; i < kK1Tok; i += 2)
                 mxv[(i >> 1) & 3] = fmaxf(mxv[(i >> 1) & 3], fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
             const float mx = fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3]));
-            if (threadIdx.x == 0) K1_TRACE(10, n);
+            if (threadIdx.x == 0) K1_TRACE_DEP(10, n, mx);
             // lazy reference max: move it (and rescale O) only when a row's max grew by > 2^8
             const bool grow = mx * c2 > m_ref + kRescaleThreshold;
             if (__any_sync(0xffffffffu, grow)) {
@@ -510,8 +521,8 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
             l += (a01.x + a01.y) + (a23.x + a23.y);
             if (hasB) ptx::mbar_arrive(&bar[EXP_DONE + 4 * x + wq]);
-            if (threadIdx.x == 0) K1_TRACE(11, n);
-            if (threadIdx.x == 128) K1_TRACE(13, n);
+            if (threadIdx.x == 0) K1_TRACE_DEP(11, n, l);
+            if (threadIdx.x == 128) K1_TRACE_DEP(13, n, l);
             if (n == 0) {  // the tile's V scale (set by the converters before their first arrive)
                 ptx::mbar_wait(&bar[V_CONV], 0);
                 s_cur = vexp[0];

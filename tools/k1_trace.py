@@ -20,7 +20,7 @@ from synth import make_config  # noqa: E402
 
 EV = ["K issued", "V issued", "QK issue", "PV issue", "V full(conv)", "V conv done",
       "S full(smax)", "pass start", "P stored", None, "pass1 done", "exp done",
-      "MMA Vconv ok", "B exp done", "B S full", "PV_B issue"]
+      "MMA Vconv ok", "B exp done", "B S full", "PV_B issue", "S loaded"]
 
 
 def main():
@@ -31,7 +31,7 @@ def main():
     plan = ld.pool.plan(ld.req_ids)
     q = wl.q(0, "cuda:0")
     out = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda:0")
-    buf = torch.zeros(16 * 64, dtype=torch.int64, device="cuda:0")
+    buf = torch.zeros(24 * 64, dtype=torch.int64, device="cuda:0")
     lib = halo.load_library()
     lib.halo_debug_k1_trace.argtypes = [ctypes.c_void_p]
     for it in range(3):
@@ -39,7 +39,7 @@ def main():
         lib.halo_debug_k1_trace(ctypes.c_void_p(buf.data_ptr()))
         plan.run_stages(0, 1, q[0], out)
         torch.cuda.synchronize()
-    t = buf.view(16, 64).cpu()
+    t = buf.view(24, 64).cpu()
     t0 = int(t[9, 0])
     print("tile0 info:", plan.export("tiles")[0].tolist())
     def at(e, n):

@@ -204,7 +204,9 @@ def setup_workload(halo, wl, dev, torch):
     lse = torch.empty((L, R, Hq), device=f"cuda:{dev}")
     ones = [1] * R
     pool.append(reqs, ones, nk, nv)
+    # plan options (defaults; the env knobs are for A/B runs of bench.py only)
     popt = halo.PlanOptions(0, 0, int(os.environ.get("HALO_MAX_SPLITS", "0")), int(os.environ.get("HALO_K2_CHUNK", "0")))
+    popt.k2_tail_pct = int(os.environ.get("HALO_K2_TAIL", "0"))
     plan = pool.plan(reqs, popt)
     info = plan.info()
     stream = torch.cuda.current_stream()

@@ -167,6 +167,10 @@ typedef struct {
                                 of the SMs (K2); 0 = default 0.65, < 0 = off   */
     float k2_early_weight;   /* work weight of K2 warps that start beside K1 (on SMs K1
                                 leaves idle); 0 = default (1.2 when the K1 rule applies) */
+    int32_t k2_tail_pct;     /* > 0: K2's last k2_tail_pct % of blocks are cut into small
+                                pieces that warps claim dynamically once their static share
+                                is done; <= 0: off (default: measured slower at C1)        */
+    int32_t reserved;
 } halo_plan_options;
 
 /* Build (or rebuild in place, when *inout != NULL) the plan of one decode step for the

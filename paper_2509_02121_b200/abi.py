@@ -30,7 +30,8 @@ class PoolConfig(C.Structure):
 class PlanOptions(C.Structure):
     _fields_ = [("min_tensor_rows", _i32), ("force_splits", _i32), ("max_splits", _i32),
                 ("k2_chunk_blocks", _i32), ("k2_shape", _i32), ("k2_sms", _i32),
-                ("k1_sm_frac", C.c_float), ("k2_early_weight", C.c_float)]
+                ("k1_sm_frac", C.c_float), ("k2_early_weight", C.c_float),
+                ("k2_tail_pct", _i32), ("reserved", _i32)]
 
 
 class PlanInfo(C.Structure):

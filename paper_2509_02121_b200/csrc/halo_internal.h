@@ -16,6 +16,7 @@ constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N 
 // few per warp and whole units divide evenly over 7 warps per SM: no stream-K pieces).
 constexpr int kK2WarpsWide = 12, kK2StagesWide = 2;
 constexpr int kK2WarpsNarrow = 7, kK2StagesNarrow = 4;
+constexpr int kK2HeadPad = 8;       // K2's MMA N dimension: the g q-heads of a unit padded to 8
 constexpr int kBlkCountShift = 27;  // K2 block entry: block | (ntok-1) << 27 (| unit start << 31)
 constexpr uint32_t kBlkMask = (1u << kBlkCountShift) - 1;
 
@@ -68,10 +69,27 @@ struct PlanDev {
     const int32_t *unit_nseg;    // [nunits]
     const int32_t *unit_seg;     // [nunits] first scratch slot (-1 if nseg == 1)
     int32_t *unit_count;         // [nunits] arrival counters (zero between launches)
-    float *seg_o;                // [nseg_total][g][D]  unnormalised o (base-2 state)
-    float *seg_ml;               // [nseg_total][g][2]  (m, l)
+    float *seg_o;                // [nseg_total][8 heads x D] unnormalised o (base-2 state), K2 fragment layout
+    float *seg_ml;               // [nseg_total][8][2]  (m, l) per head
     int32_t ntiles, nreq, nunits, max_slots, nwarps, nchunks, nblocks;
     int32_t k2_warps;            // K2 warps per CTA: kK2WarpsWide or kK2WarpsNarrow
+    // static-then-dynamic K2 schedule: warp w streams static chunk w, then claims chunks
+    // dyn_first, dyn_first + 1, ... from dyn_counter[layer % 4] (the last claimant resets it);
+    // dyn_first == nchunks: static round-robin (warp w takes chunks w, w + nwarps, ...)
+    int32_t dyn_first;
+    int32_t *dyn_counter;
+    // K1 -> K2 completion hint (per layer slot layer % 4): every K1 CTA adds 1 to
+    // k1_done[slot] when its partials are written (release); K2 reads it (acquire) to decide
+    // whether a finished unit can merge now or is parked until K1 completes; K2's last warp
+    // (k2_done) resets both.  Correctness never rests on it (K2 still calls
+    // griddepcontrol.wait before any output write).
+    uint32_t *k1_done;           // [4]
+    uint32_t *k2_done;           // [4]
+    // K2 scratch per layer slot (a K2 launch may overlap the previous layer's): stream-K
+    // pieces, unit arrival counters and parked unit states are at slot * stride.
+    int64_t seg_slot_stride;     // floats between the slots of seg_o (seg_ml likewise, /D*2)
+    int32_t count_slot_stride;   // ints between the slots of unit_count
+    float *park;                 // [4][nunits][g * (D + 2)]: o (fragment layout), then (m, l) per head
 };
 
 struct PoolGeom {
@@ -95,10 +113,11 @@ cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tma
                                const CUtensorMap *tmap_k8, const CUtensorMap *tmap_v8,
                                const CUtensorMap *tmap_q, const PlanDev &p, const PoolGeom &g,
                                int layer, const void *q, float scale, cudaStream_t s);
-// K2+K3: paged-suffix decode with the fused log-sum-exp merge of the K1 partials.
-cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void *pool_k,
-                                 const void *pool_v, int layer, const void *q, float *out,
-                                 float *lse, float scale, int num_sms, cudaStream_t s);
+// K2+K3: paged-suffix decode with the fused log-sum-exp merge of the K1 partials.  K/V slabs
+// arrive by TMA through the pool's one-block tensor maps (tmap_k / tmap_v, 128-B swizzle).
+cudaError_t launch_suffix_decode(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v, const PlanDev &p,
+                                 const PoolGeom &g, int layer, const void *q, float *out, float *lse,
+                                 float scale, cudaStream_t s);
 // K5 / K4-unpack: rows src[layer][i][head][:] -> pool slot slots[i] (i < n_copy); slots
 // [n_copy, n_copy+n_zero) are zero-filled.  src has `src_rows` rows per layer.
 // tags[i] (nullable: no V-table update) = allocation epoch of slot i's block.

@@ -92,6 +92,7 @@ struct PrefixArgs {
     int32_t tma_q;      // tmq is valid: tiles with consecutive requests load Q by TMA
     const uint64_t *vmax;  // the pool's V table [layer][block] (low 16 bits: bf16 max |V|)
     int64_t cap;
+    int32_t layer;
 };
 
 template <int D>
@@ -574,6 +575,10 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
     }
 done:
     __syncthreads();
+    // completion hint for K2 (PlanDev::k1_done): this tile's partials are written (the barrier
+    // orders every thread's stores before thread 0's release)
+    if (threadIdx.x == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.p.k1_done + (a.layer & 3)) : "memory");
     if (warp == 9) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 512);
@@ -625,6 +630,7 @@ cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tma
     a.tma_q = tmap_q != nullptr ? 1 : 0;
     a.vmax = g.vmax;
     a.cap = g.cap;
+    a.layer = layer;
     const CUtensorMap *tq = tmap_q != nullptr ? tmap_q : tmap_k;  // unused when tma_q == 0
     if (g.d == 128) return launch_t<128>(tmap_k, tmap_v, tmap_k8, tmap_v8, tq, a, s);
     if (g.d == 64) return launch_t<64>(tmap_k, tmap_v, tmap_k8, tmap_v8, tq, a, s);

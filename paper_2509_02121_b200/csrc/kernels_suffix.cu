@@ -56,189 +56,148 @@ extern "C" int halo_debug_k2_trace(void *buf) {
 namespace halo {
 namespace {
 
-#ifndef HALO_K2_QK_BF16
-#define HALO_K2_QK_BF16 0  // 1: q.k with mixed-precision bf16 FMAs (no K conversion, q kept as bf16)
-#endif
-
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLazy = 8.f;  // base-2 headroom of the lazy running max (p <= 2^8)
+constexpr int NPAD = kK2HeadPad;  // MMA N: the unit's g q-heads padded to 8
+constexpr int NPARK = 16;         // units a warp may park while K1 is still running
+#ifndef HALO_K2_PF
+#define HALO_K2_PF 0              // blocks prefetched into L2 ahead of the smem ring (A/B: 2-8 slower, tools/k1k2_cosched_sweep.py)
+#endif
 
 struct SuffixArgs {
     PlanDev p;
-    const uint16_t *pool_k, *pool_v;  // bf16 bits
-    int64_t layer_off;                // elements to this layer in the pool
+    int64_t layer_blk;                // layer * cap (4th TMA coordinate offset)
     const uint16_t *q;                // [nreq][hq][D]
     float *out, *lse;
     int32_t hkv, hq;
     float qscale;                     // scale * log2(e)
+    int32_t layer;                    // selects the dynamic-claim counter (layer % 4)
 };
-
-constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 template <int D, int G, int kWarps, int kStages>
 struct Shape {
-    static constexpr int LPT = cmax(2, cmax(G, G * D / 64));  // lanes per token row
-    static constexpr int TPI = 32 / LPT;                      // tokens per warp iteration
-    static constexpr int NIT = kBlockTok / TPI;
-    static constexpr int NCH = D / (8 * LPT);                 // 16-B chunks per lane per row (q.k)
+    static constexpr int KS = D / 16;                         // k-steps of q.k = m-tiles of P.V
+    static constexpr int ATOMS = D / 64;                      // 128-B swizzle atoms per row
     static constexpr int SLAB = kBlockTok * D * 2;            // bytes of one (block, head) slab
-    static constexpr int STAGE = 2 * SLAB;                    // K + V
+    static constexpr int STAGE = 2 * SLAB;                    // K + V (multiple of 1024)
     static constexpr int QB = G * D * 2;                      // the unit's q rows (bf16)
-    // ring stages / q buffers: kStages and 2 unless the warps' rings would not fit in 227 KB
-    static constexpr bool fits(int st, int qn) {
-        return kWarps * (st * STAGE + qn * QB + kBlockTok * G * 4 + 256) <= 227 * 1024;
-    }
-    static constexpr int ST = fits(kStages, 1) ? kStages : kStages - 1;
+    // per-warp misc area: q buffers, alpha, token counts, chunk FIFO, barriers
+    static constexpr int misc(int st, int qn) { return (qn * QB + 8 * 4 + st * 4 + 8 * 4 + NPARK * 4 + (st + 2) * 8 + 127) / 128 * 128; }
+    static constexpr bool fits(int st, int qn) { return st >= 1 && kWarps * (st * STAGE + misc(st, qn)) <= 227 * 1024; }
+    // ring stages / q buffers: kStages and 2 unless the warps' areas would not fit in 227 KB
+    static constexpr int ST = fits(kStages, 1) ? kStages : fits(kStages - 1, 1) ? kStages - 1 : kStages - 2;
     static constexpr int QN = fits(ST, 2) ? 2 : 1;
-    static constexpr int OFF_Q = ST * STAGE;
-    static constexpr int OFF_PS = OFF_Q + QN * QB;
-    static constexpr int OFF_ALPH = OFF_PS + kBlockTok * G * 4;
+    static constexpr int MISC = misc(ST, QN);
+    static constexpr int OFF_MISC = kWarps * ST * STAGE;      // stages of all warps first (1024-aligned)
+    static constexpr int OFF_Q = 0;                           // within the misc area
+    static constexpr int OFF_ALPH = OFF_Q + QN * QB;
     static constexpr int OFF_NT = OFF_ALPH + 8 * 4;
-    static constexpr int OFF_BAR = (OFF_NT + ST * 4 + 7) / 8 * 8;
-    static constexpr int WARP_SMEM = OFF_BAR + (ST + 2) * 8;
-    static constexpr int WARP_SMEM_AL = (WARP_SMEM + 127) / 128 * 128;
-    static_assert(G <= LPT && LPT <= 16 && NCH >= 1 && NIT >= 1, "lane mapping");
-    static_assert(ST >= 2 && kWarps * WARP_SMEM_AL <= 227 * 1024, "K2 shared memory");
-    static_assert(NCH * 8 * LPT == D, "d must split into 16-B chunks over the row lanes");
+    static constexpr int OFF_CQ = OFF_NT + ST * 4;
+    static constexpr int OFF_PARK = OFF_CQ + 8 * 4;               // [NPARK] parked units
+    static constexpr int OFF_BAR = (OFF_PARK + NPARK * 4 + 7) / 8 * 8;
+    static constexpr int SMEM = OFF_MISC + kWarps * MISC;
+    static_assert(ST >= 2 && SMEM <= 227 * 1024, "K2 shared memory");
+    static_assert(STAGE % 1024 == 0 && G <= NPAD && D % 64 == 0, "K2 shape");
 };
 
-// Sum each of v[0..G) over the LPT lanes of a token group; afterwards lane c holds the
-// full sum of head c / (LPT/G) in v[0].  Every lane of a head computes the same pairwise
-// sums, so the replicas are bit-identical.
-template <int G, int LPT>
-__device__ __forceinline__ float transpose_reduce(float (&v)[G], int c) {
-    int mask = LPT / 2;
-#pragma unroll
-    for (int lvl = 0; (G >> lvl) > 1; ++lvl) {
-        const int half = (G >> lvl) / 2;
-        const bool upper = (c & mask) != 0;
-#pragma unroll
-        for (int i = 0; i < half; ++i) {
-            const float keep = upper ? v[i + half] : v[i];
-            const float send = upper ? v[i] : v[i + half];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-        }
-        mask >>= 1;
-    }
-#pragma unroll
-    for (int m = LPT / G / 2; m >= 1; m >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
-    return v[0];
+// Byte offset of (token r, dim d) in a (block, head) slab loaded by TMA with 128-B swizzle:
+// atom d/64 of 16 rows x 128 B; 16-B chunk c of row r sits at chunk c ^ (r % 8).
+__device__ __forceinline__ uint32_t swz(int r, int d) {
+    return (uint32_t)((d >> 6) * (kBlockTok * 128) + r * 128 + ((((d & 63) >> 3) ^ (r & 7)) << 4));
 }
 
-template <int D, int G>
-using QAcc = float2[G][Shape<D, G, 1, 2>::NCH][4];  // q.k mapping: G heads x this lane's row chunks
-template <int D, int G>
-using OAcc = float2[G][D / 64];               // P.V mapping: G heads x this lane's D/32 dims
-
-// DPL = D/32 consecutive floats at p (16-B or 8-B aligned) <-> float2 pairs
-template <int NP>
-__device__ __forceinline__ void ld_pairs(const float *p, float2 (&x)[NP]) {
-    if constexpr (NP == 2) {
-        const float4 v = *reinterpret_cast<const float4 *>(p);
-        x[0] = make_float2(v.x, v.y);
-        x[1] = make_float2(v.z, v.w);
-    } else {
-        x[0] = *reinterpret_cast<const float2 *>(p);
-    }
-}
-template <int NP>
-__device__ __forceinline__ void ld_pairs_cg(const float *p, float2 (&x)[NP]) {
-    if constexpr (NP == 2) {
-        const float4 v = __ldcg(reinterpret_cast<const float4 *>(p));
-        x[0] = make_float2(v.x, v.y);
-        x[1] = make_float2(v.z, v.w);
-    } else {
-        x[0] = __ldcg(reinterpret_cast<const float2 *>(p));
-    }
-}
-template <int NP>
-__device__ __forceinline__ void st_pairs(float *p, const float2 (&x)[NP], float sc) {
-    if constexpr (NP == 2) {
-        *reinterpret_cast<float4 *>(p) = make_float4(x[0].x * sc, x[0].y * sc, x[1].x * sc, x[1].y * sc);
-    } else {
-        *reinterpret_cast<float2 *>(p) = make_float2(x[0].x * sc, x[0].y * sc);
-    }
-}
-
-// Final merge of a unit's suffix state (base-2 max mh, sum lh, unnormalised o) with the
-// request's K1 partials, then the fp32 output / lse store.  All lanes: lane owns dims
-// [lane*D/32, (lane+1)*D/32) of the G heads.
+// Final merge of a unit's suffix state with the request's K1 partials, then the fp32 output /
+// lse store.  Lane layout (the P.V MMA's accumulator): lane (g = lane/4, c = lane%4) holds, for
+// heads h_e = 2c + e (e = 0, 1) and dims d = 16t + g + 8j, o[t][2j + e].  mh/lh: base-2 running
+// max and the (lane-reduced) sum of the two heads.
 template <int D, int G>
 __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head, int nslots, int lane,
-                                         const float (&mh)[G], const float (&lh)[G], OAcc<D, G> &o2,
-                                         const float (&lse0)[G], bool have0) {
-    constexpr int NP = D / 64, DPL = D / 32;
+                                         const float (&mh)[2], const float (&lh)[2], float (&o)[D / 16][4],
+                                         const float (&lse0)[2], bool have0) {
+    constexpr int KS = D / 16;
     const PlanDev &P = a.p;
-    float M[G], L[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) M[h] = (lh[h] > 0.f) ? mh[h] + __log2f(lh[h]) : -INFINITY;
+    const int g = lane >> 2, c = lane & 3;
     const int64_t slot_stride = (int64_t)P.nreq * a.hq;
     const int64_t row0 = (int64_t)req * a.hq + head * G;
+    float M[2], L[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int h = 2 * c + e;
+        M[e] = (lh[e] > 0.f) ? mh[e] + __log2f(lh[e]) : -INFINITY;
+        if (h < G)
+            for (int sl = 0; sl < nslots; ++sl)
+                M[e] = fmaxf(M[e], (sl == 0 && have0 ? lse0[e] : P.part_lse[sl * slot_stride + row0 + h]) * kLog2e);
+        const float ws = (lh[e] > 0.f) ? ptx::ex2(mh[e] - M[e]) : 0.f;
+        L[e] = lh[e] * ws;
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+            o[t][e] *= ws;
+            o[t][2 + e] *= ws;
+        }
+    }
     for (int sl = 0; sl < nslots; ++sl) {
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-            M[h] = fmaxf(M[h], (sl == 0 && have0 ? lse0[h] : P.part_lse[sl * slot_stride + row0 + h]) * kLog2e);
-    }
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-        const float ws = (lh[h] > 0.f) ? ptx::ex2(mh[h] - M[h]) : 0.f;
-        L[h] = lh[h] * ws;
-#pragma unroll
-        for (int i = 0; i < NP; ++i) o2[h][i] = ptx::fmul2(o2[h][i], make_float2(ws, ws));
-    }
-    for (int sl = 0; sl < nslots; ++sl) {
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
+        for (int e = 0; e < 2; ++e) {
+            const int h = 2 * c + e;
+            if (h >= G) continue;
             const int64_t row = sl * slot_stride + row0 + h;
-            const float w = ptx::ex2((sl == 0 && have0 ? lse0[h] : P.part_lse[row]) * kLog2e - M[h]);
-            L[h] += w;
-            float2 x[NP];
-            ld_pairs<NP>(P.part_o + row * D + lane * DPL, x);
+            const float w = ptx::ex2((sl == 0 && have0 ? lse0[e] : P.part_lse[row]) * kLog2e - M[e]);
+            L[e] += w;
+            const float *src = P.part_o + row * D + g;
 #pragma unroll
-            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(w, w), x[i], o2[h][i]);
+            for (int t = 0; t < KS; ++t) {
+                o[t][e] = fmaf(w, src[16 * t], o[t][e]);
+                o[t][2 + e] = fmaf(w, src[16 * t + 8], o[t][2 + e]);
+            }
         }
     }
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-        st_pairs<NP>(a.out + (row0 + h) * D + lane * DPL, o2[h], 1.f / L[h]);
-        if (a.lse != nullptr && lane == h) a.lse[row0 + h] = (M[h] + __log2f(L[h])) * kLn2;
+    for (int e = 0; e < 2; ++e) {
+        const int h = 2 * c + e;
+        if (h >= G) continue;
+        const float inv = 1.f / L[e];
+        float *dst = a.out + (row0 + h) * D + g;
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+            dst[16 * t] = o[t][e] * inv;
+            dst[16 * t + 8] = o[t][2 + e] * inv;
+        }
+        if (a.lse != nullptr && g == 0) a.lse[row0 + h] = (M[e] + __log2f(L[e])) * kLn2;
     }
 }
 
 template <int D, int G, int kWarps, int kStages>
-__global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const SuffixArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 1)
+suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                     const SuffixArgs a) {
     using S = Shape<D, G, kWarps, kStages>;
-    constexpr int LPT = S::LPT, TPI = S::TPI, NIT = S::NIT, NCH = S::NCH, ST = S::ST;
-    constexpr int NP = D / 64, DPL = D / 32;
-    extern __shared__ __align__(128) uint8_t smem_raw[];
+    constexpr int KS = S::KS, ST = S::ST;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t *ws = smem_raw + warp * S::WARP_SMEM_AL;
-    uint8_t *qbuf = ws + S::OFF_Q;
-    float *ps = reinterpret_cast<float *>(ws + S::OFF_PS);
-    float *alph = reinterpret_cast<float *>(ws + S::OFF_ALPH);
-    int32_t *snt = reinterpret_cast<int32_t *>(ws + S::OFF_NT);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ws + S::OFF_BAR);
+    uint8_t *stages = smem_raw + warp * ST * S::STAGE;
+    uint8_t *ms = smem_raw + S::OFF_MISC + warp * S::MISC;
+    uint8_t *qbuf = ms + S::OFF_Q;
+    float *alph = reinterpret_cast<float *>(ms + S::OFF_ALPH);
+    int32_t *snt = reinterpret_cast<int32_t *>(ms + S::OFF_NT);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ms + S::OFF_BAR);
     uint64_t *qbar = full + ST;
+    (void)alph;
 
     if (lane == 0) {
         for (int s = 0; s < ST; ++s) ptx::mbar_init(&full[s], 1);
-        ptx::mbar_init(&qbar[0], 1);
-        ptx::mbar_init(&qbar[1], 1);
+        for (int i = 0; i < S::QN; ++i) ptx::mbar_init(&qbar[i], 1);
         ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tmk);
+        ptx::prefetch_tmap(&tmv);
     }
     __syncwarp();
 
     const PlanDev &P = a.p;
-    const int tg = lane / LPT;   // token group within the warp
-    const int c = lane % LPT;    // lane within the row
-    const int hsel = c / (LPT / G);
-    const bool head_writer = (c % (LPT / G)) == 0;
+    const int g = lane >> 2, c = lane & 3;
     const int gw = blockIdx.x * kWarps + warp;
     if (gw >= P.nwarps) return;
     K2_TRACE(gw, 0);
-    const uint16_t *pk = a.pool_k + a.layer_off;
-    const uint16_t *pv = a.pool_v + a.layer_off;
 
     // ---- producer (all lanes track the state; lane 0 issues the copies) ----
     // PDL: the next kernel in the stream (the next layer's K1) may start its prologue now;
@@ -251,6 +210,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
         px = pstart = ci.x;
         phi = ci.y;
     }
+    // static-then-dynamic schedule (optional, halo_plan_options.k2_tail_pct): after its static
+    // chunk the warp claims chunks from a per-layer counter; the next claim is issued when a
+    // chunk starts (lane 0 holds the result).  Chunk ids go through a small per-warp FIFO from
+    // the producer (fill) to the consumer loop.
+    const bool dyn = P.dyn_first < P.nchunks;
+    const int ndyn = P.nchunks - P.dyn_first;
+    int32_t *dcount = P.dyn_counter + (a.layer & 3);
+    int32_t *cq = reinterpret_cast<int32_t *>(ms + S::OFF_CQ);
+    uint32_t cq_w = 0, cq_r = 0;
+    bool prod_done = false;
+    int claim = 0;
+    if (dyn) {
+        if (lane == 0) {
+            cq[0] = gw;
+            claim = atomicAdd(dcount, 1);
+        }
+        cq_w = 1;
+    }
     uint32_t p_count = 0, c_count = 0, q_issued = 0, q_read = 0;
     int eb = -64;                       // base index of the descriptor batch in `ent`
     uint2 ent = make_uint2(0, 0), ent_next = make_uint2(0, 0);
@@ -259,10 +236,26 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
     };
     auto fill = [&]() {
         while (p_count - c_count < (uint32_t)ST) {
-            if (px >= phi) {  // this warp's next chunk (only with more chunks than warps)
-                if (pch >= P.nchunks) break;
-                pch += P.nwarps;
-                if (pch >= P.nchunks) break;
+            if (px >= phi) {  // this warp's next chunk
+                if (!dyn) {   // static round-robin (only with more chunks than warps)
+                    if (pch >= P.nchunks) break;
+                    pch += P.nwarps;
+                    if (pch >= P.nchunks) break;
+                } else {
+                    if (prod_done || cq_w - cq_r >= 8) break;
+                    const int k = __shfl_sync(0xffffffffu, claim, 0);
+                    if (k >= ndyn) {  // no work left; the launch's last claim resets the counter
+                        prod_done = true;
+                        if (lane == 0 && k == ndyn + P.nwarps - 1) atomicExch(dcount, 0);
+                        break;
+                    }
+                    pch = P.dyn_first + k;
+                    if (lane == 0) {
+                        cq[cq_w & 7] = pch;
+                        claim = atomicAdd(dcount, 1);  // the claim after this one, in flight
+                    }
+                    ++cq_w;
+                }
                 const int4 c2 = P.chunk_info[pch];
                 px = pstart = c2.x;
                 phi = c2.y;
@@ -292,26 +285,47 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             const int st = p_count % ST;
             if (lane == 0) {
                 snt[st] = (int)((ex >> kBlkCountShift) & 15u) + 1;
-                const int64_t off = (int64_t)(ex & kBlkMask) * (kBlockTok * D);
-                uint8_t *dst = ws + st * S::STAGE;
+                const uint32_t slab = ex & kBlkMask;
+                const int blk = (int)(slab / (uint32_t)a.hkv), hd = (int)(slab % (uint32_t)a.hkv);
+                const int c3 = (int)(a.layer_blk + blk);
+                uint8_t *dst = stages + st * S::STAGE;
                 ptx::mbar_arrive_expect_tx(&full[st], S::STAGE);
-#ifndef HALO_K2_NO_L2_HINT
-                // suffix K/V is read exactly once: an L2 evict_first policy keeps K1's
-                // partials, q and the plan resident in L2 (C1 3.75 -> 4.02 M queries/s).
-                // Blocks of folded prefix nodes (bit 31 of the entry) are read by several
-                // units and keep the default policy.
+                // K and V slabs by TMA in the 128-B swizzle the ldmatrix reads expect.  Suffix
+                // K/V is read exactly once: L2 evict_first keeps K1's partials, q and the plan
+                // resident (C1 3.75 -> 4.02 M queries/s, round 1); blocks of folded prefix nodes
+                // (bit 31 of the entry) are read by several units and keep the default policy.
                 if (ey >> 31) {
-                    ptx::bulk_g2s(dst, pk + off, S::SLAB, &full[st]);
-                    ptx::bulk_g2s(dst + S::SLAB, pv + off, S::SLAB, &full[st]);
+#pragma unroll
+                    for (int at = 0; at < S::ATOMS; ++at) {
+                        ptx::tma_load_4d(dst + at * (kBlockTok * 128), &tmk, at * 64, 0, hd, c3, &full[st]);
+                        ptx::tma_load_4d(dst + S::SLAB + at * (kBlockTok * 128), &tmv, at * 64, 0, hd, c3, &full[st]);
+                    }
                 } else {
                     const uint64_t pol = ptx::l2_policy_evict_first();
-                    ptx::bulk_g2s_hint(dst, pk + off, S::SLAB, &full[st], pol);
-                    ptx::bulk_g2s_hint(dst + S::SLAB, pv + off, S::SLAB, &full[st], pol);
+#pragma unroll
+                    for (int at = 0; at < S::ATOMS; ++at) {
+                        ptx::tma_load_4d_hint(dst + at * (kBlockTok * 128), &tmk, at * 64, 0, hd, c3, &full[st], pol);
+                        ptx::tma_load_4d_hint(dst + S::SLAB + at * (kBlockTok * 128), &tmv, at * 64, 0, hd, c3,
+                                              &full[st], pol);
+                    }
                 }
-#else
-                ptx::bulk_g2s(dst, pk + off, S::SLAB, &full[st]);
-                ptx::bulk_g2s(dst + S::SLAB, pv + off, S::SLAB, &full[st]);
-#endif
+            }
+            // L2 prefetch HALO_K2_PF blocks ahead (same chunk): the ring's smem stages cap the
+            // bytes a warp has in flight; prefetched blocks raise it without holding smem, so
+            // the SMs left free beside K1 can stream closer to HBM speed
+            if (HALO_K2_PF > 0 && px + HALO_K2_PF < phi) {
+                const int jp = px + HALO_K2_PF - eb;  // < 64: within ent / ent_next
+                const uint32_t pex = jp < 32 ? __shfl_sync(0xffffffffu, ent.x, jp)
+                                             : __shfl_sync(0xffffffffu, ent_next.x, jp - 32);
+                if (lane == 0) {
+                    const uint32_t slab = pex & kBlkMask;
+                    const int blk = (int)(slab / (uint32_t)a.hkv), hd = (int)(slab % (uint32_t)a.hkv);
+#pragma unroll
+                    for (int at = 0; at < S::ATOMS; ++at) {
+                        ptx::tma_prefetch_4d(&tmk, at * 64, 0, hd, (int)(a.layer_blk + blk));
+                        ptx::tma_prefetch_4d(&tmv, at * 64, 0, hd, (int)(a.layer_blk + blk));
+                    }
+                }
             }
             ++px;
             ++p_count;
@@ -330,7 +344,126 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             k1_ready = true;
         }
     };
-    for (int cc = gw; cc < P.nchunks; cc += P.nwarps) {
+    // this layer slot's scratch (a K2 launch may overlap the previous layer's)
+    const int ls = a.layer & 3;
+    float *seg_o = P.seg_o + ls * P.seg_slot_stride;
+    float *seg_ml = P.seg_ml + ls * P.seg_slot_stride;
+    int32_t *unit_count = P.unit_count + ls * P.count_slot_stride;
+    constexpr int PARK_UNIT = G * (D + 2);
+    float *park = P.park + (int64_t)ls * P.nunits * PARK_UNIT;
+    int32_t *plist = reinterpret_cast<int32_t *>(ms + S::OFF_PARK);
+    int npark = 0;
+    // has K1 finished (all its CTAs published)?  A hint only: outputs are written after
+    // griddepcontrol.wait either way.
+    auto k1_hint = [&]() -> bool {
+        if (k1_ready) return true;
+        uint32_t v = 0;
+        if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.k1_done + ls) : "memory");
+        v = __shfl_sync(0xffffffffu, v, 0);
+        return v >= (uint32_t)P.ntiles;
+    };
+    // merge every stream-K piece of unit u (in segment order: deterministic) and finalize
+    auto merge_pieces = [&](int u) {
+        const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
+        const int req = m0.z, head = m0.w, nslots = m1.x, nseg = m1.y, base = m1.z;
+        float lseM[2] = {0.f, 0.f};
+        const bool haveM = nslots > 0;
+        if (haveM) {
+            const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (2 * c + e < G) lseM[e] = __ldcg(src + 2 * c + e);
+        }
+        float M[2] = {-INFINITY, -INFINITY}, L[2] = {0.f, 0.f};
+        float o[KS][4];
+#pragma unroll
+        for (int t = 0; t < KS; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+        if (2 * c < G) {
+            for (int sg = 0; sg < nseg; ++sg)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (2 * c + e < G)
+                        M[e] = fmaxf(M[e], __ldcg(seg_ml + ((int64_t)(base + sg) * NPAD + 2 * c + e) * 2));
+            for (int sg = 0; sg < nseg; ++sg) {
+                float w[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    w[e] = 0.f;
+                    if (2 * c + e < G) {
+                        const float2 ml = __ldcg(reinterpret_cast<const float2 *>(
+                            seg_ml + ((int64_t)(base + sg) * NPAD + 2 * c + e) * 2));
+                        w[e] = (ml.y > 0.f) ? ptx::ex2(ml.x - M[e]) : 0.f;
+                        L[e] += ml.y * w[e];
+                    }
+                }
+                const float *src = seg_o + (int64_t)(base + sg) * (NPAD * D) + lane * (4 * KS);
+#pragma unroll
+                for (int t = 0; t < KS; ++t) {
+                    const float4 x = __ldcg(reinterpret_cast<const float4 *>(src + 4 * t));
+                    o[t][0] = fmaf(w[0], x.x, o[t][0]);
+                    o[t][1] = fmaf(w[1], x.y, o[t][1]);
+                    o[t][2] = fmaf(w[0], x.z, o[t][2]);
+                    o[t][3] = fmaf(w[1], x.w, o[t][3]);
+                }
+            }
+        }
+        finalize<D, G>(a, req, head, nslots, lane, M, L, o, lseM, haveM);
+    };
+    // wait for K1, then merge the parked units (whole units from `park`, stream-K ones from
+    // their pieces) in parking order
+    auto drain = [&]() {
+        wait_k1();
+        __syncwarp();
+        for (int i = 0; i < npark; ++i) {
+            const int ent = plist[i];
+            const int u = ent & 0x7fffffff;
+            if (ent < 0) {
+                merge_pieces(u);
+                continue;
+            }
+            const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
+            const float *pk = park + (int64_t)u * PARK_UNIT;
+            float o[KS][4], mm[2] = {-INFINITY, -INFINITY}, ll[2] = {0.f, 0.f};
+#pragma unroll
+            for (int t = 0; t < KS; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int h = 2 * c + e;
+                if (h >= G) continue;
+#pragma unroll
+                for (int t = 0; t < KS; ++t) {
+                    o[t][e] = __ldcg(pk + h * D + 16 * t + g);
+                    o[t][2 + e] = __ldcg(pk + h * D + 16 * t + g + 8);
+                }
+                const float2 ml = __ldcg(reinterpret_cast<const float2 *>(pk + G * D + 2 * h));
+                mm[e] = ml.x;
+                ll[e] = ml.y;
+            }
+            const float z[2] = {0.f, 0.f};
+            finalize<D, G>(a, m0.z, m0.w, m1.x, lane, mm, ll, o, z, false);
+        }
+        __syncwarp();
+        npark = 0;
+    };
+    // per-lane ldmatrix row addresses within a slab: K (A operand, row = token) and V^T
+    // (A operand via .trans, memory row = token); matrix m = lane / 8, row lane % 8
+    const int lm = lane >> 3, lr = lane & 7;
+    const int k_tok = lr + 8 * (lm & 1), k_d = 8 * (lm >> 1);   // K: a0..a3 = (tok 0-7 | 8-15) x (d +0 | +8)
+    const int v_tok = lr + 8 * (lm >> 1), v_d = 8 * (lm & 1);   // V^T: a0..a3 = (d +0 | +8) x (tok 0-7 | 8-15)
+    const int e_src = 8 * c + (g >> 1);  // lane holding p(token 2c, head g) (and 2c+1 at +4)
+    for (uint32_t ck = 0;; ++ck) {
+        int cc;
+        if (!dyn) {
+            cc = gw + (int)ck * P.nwarps;
+            if (cc >= P.nchunks) break;
+        } else {
+            while (cq_w <= ck && !prod_done) fill();  // the producer decides the next chunk
+            if (ck >= cq_w) break;
+            __syncwarp();
+            cc = cq[ck & 7];
+            __syncwarp();
+            cq_r = ck + 1;
+        }
         const int4 cinfo = cc == gw ? ci : P.chunk_info[cc];
         const int lo = cinfo.x, hi = cinfo.y;
         const int u_begin = cinfo.z, u_end = cinfo.w;
@@ -340,48 +473,30 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
             const int req = m0.z, head = m0.w;
             // once K1 is known complete, the merge's first partial lse is loaded now and
             // lands while the unit streams (the merge otherwise waits one L2 round trip)
-            float lse0[G];
+            float lse0[2] = {0.f, 0.f};
             const bool have0 = k1_ready && m1.x > 0 && m1.y == 1;
             if (have0) {
                 const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
 #pragma unroll
-                for (int h = 0; h < G; ++h) lse0[h] = __ldcg(src + h);
-            } else {
-#pragma unroll
-                for (int h = 0; h < G; ++h) lse0[h] = 0.f;
+                for (int e = 0; e < 2; ++e)
+                    if (2 * c + e < G) lse0[e] = __ldcg(src + 2 * c + e);
             }
-            OAcc<D, G> o2;
+            // O^T accumulators (d x 8 heads, MMA C layout), running max / lane-partial sums
+            float o[KS][4];
 #pragma unroll
-            for (int h = 0; h < G; ++h)
-#pragma unroll
-                for (int i = 0; i < NP; ++i) o2[h][i] = make_float2(0.f, 0.f);
-            float m = -INFINITY, l = 0.f;
+            for (int t = 0; t < KS; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+            float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
             if (xs < xe) {
-                // q rows of the g heads, this lane's dims, pre-scaled (waits for the bulk copy)
-#if HALO_K2_QK_BF16
-                uint32_t qw[G][NCH][4];  // raw bf16 pairs (scale applied to the score)
-#else
-                QAcc<D, G> q2;           // fp32, pre-scaled
-#endif
+                // q^T as the B operand of q.k: b0 = q[head g][16s + 2c, +1], b1 = +8 (0 for g >= G)
+                uint32_t qf[KS][2];
                 fill();
                 ptx::mbar_wait(&qbar[q_read % S::QN], (q_read / S::QN) & 1);
                 const uint8_t *qs = qbuf + (q_read % S::QN) * S::QB;
 #pragma unroll
-                for (int h = 0; h < G; ++h)
-#pragma unroll
-                    for (int k = 0; k < NCH; ++k) {
-                        const uint4 raw = *reinterpret_cast<const uint4 *>(qs + h * D * 2 + (k * LPT + c) * 16);
-                        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-#if HALO_K2_QK_BF16
-                            qw[h][k][i] = w[i];
-#else
-                            const float2 f = ptx::bf2_to_f2(w[i]);
-                            q2[h][k][i] = make_float2(f.x * a.qscale, f.y * a.qscale);
-#endif
-                        }
-                    }
+                for (int t = 0; t < KS; ++t) {
+                    qf[t][0] = g < G ? *reinterpret_cast<const uint32_t *>(qs + (g * D + 16 * t + 2 * c) * 2) : 0u;
+                    qf[t][1] = g < G ? *reinterpret_cast<const uint32_t *>(qs + (g * D + 16 * t + 8 + 2 * c) * 2) : 0u;
+                }
                 __syncwarp();
                 ++q_read;
 
@@ -393,115 +508,84 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                     if (c_count == 0) K2_TRACE(gw, 1);
 #endif
                     const int ntok = snt[st];
-                    const uint8_t *kb = ws + st * S::STAGE;
-                    const uint8_t *vb = kb + S::SLAB;
+                    const uint32_t kb = ptx::smem_u32(stages + st * S::STAGE);
+                    const uint32_t vb = kb + S::SLAB;
 
-                    // ---- scores: lane (tg, c) ends with head hsel's score of token it*TPI+tg
-                    float s[NIT];
+                    // ---- S^T (16 tokens x 8 heads) = K . q^T on the tensor cores ----
+                    float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int it = 0; it < NIT; ++it) {
-                        const int t = it * TPI + tg;
-                        float2 acc[G];
-#pragma unroll
-                        for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
-#pragma unroll
-                        for (int k = 0; k < NCH; ++k) {
-                            const uint4 raw = *reinterpret_cast<const uint4 *>(kb + t * (D * 2) + (k * LPT + c) * 16);
-#if HALO_K2_QK_BF16
-                            const uint32_t kw[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-                            for (int h = 0; h < G; ++h)
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    acc[h].x = ptx::fma_bf16_lo(kw[i], qw[h][k][i], acc[h].x);
-                                    acc[h].y = ptx::fma_bf16_hi(kw[i], qw[h][k][i], acc[h].y);
-                                }
-#else
-                            const float2 k0 = ptx::bf2_to_f2(raw.x), k1 = ptx::bf2_to_f2(raw.y);
-                            const float2 k2 = ptx::bf2_to_f2(raw.z), k3 = ptx::bf2_to_f2(raw.w);
-#pragma unroll
-                            for (int h = 0; h < G; ++h) {
-                                acc[h] = (k == 0) ? ptx::fmul2(q2[h][k][0], k0) : ptx::ffma2(q2[h][k][0], k0, acc[h]);
-                                acc[h] = ptx::ffma2(q2[h][k][1], k1, acc[h]);
-                                acc[h] = ptx::ffma2(q2[h][k][2], k2, acc[h]);
-                                acc[h] = ptx::ffma2(q2[h][k][3], k3, acc[h]);
-                            }
-#endif
-                        }
-                        float part[G];
-#pragma unroll
-                        for (int h = 0; h < G; ++h) part[h] = acc[h].x + acc[h].y;
-#if HALO_K2_QK_BF16
-                        const float sc = transpose_reduce<G, LPT>(part, c) * a.qscale;
-#else
-                        const float sc = transpose_reduce<G, LPT>(part, c);
-#endif
-                        s[it] = (t < ntok) ? sc : -INFINITY;
+                    for (int t = 0; t < KS; ++t) {
+                        uint32_t a0, a1, a2, a3;
+                        ptx::ldsm_x4(kb + swz(k_tok, 16 * t + k_d), a0, a1, a2, a3);
+                        ptx::mma_16816(sc, a0, a1, a2, a3, qf[t][0], qf[t][1]);
                     }
-                    // ---- lazy online softmax (base 2) ----
-                    float bm = s[0];
+                    // lane holds tokens g, g+8 of heads 2c, 2c+1: scale, mask padding and the
+                    // tokens past a partial block
+                    float s4[4];
 #pragma unroll
-                    for (int it = 1; it < NIT; ++it) bm = fmaxf(bm, s[it]);
-                    if (__any_sync(0xffffffffu, bm > m + kLazy)) {
+                    for (int i = 0; i < 4; ++i) {
+                        const int tok = g + 8 * (i >> 1), hh = 2 * c + (i & 1);
+                        s4[i] = (tok < ntok && hh < G) ? sc[i] * a.qscale : -INFINITY;
+                    }
+                    // ---- lazy online softmax (base 2): rescale only when a head's block max
+                    // exceeds its running max by more than 2^8 ----
+                    const float bm0 = fmaxf(s4[0], s4[2]), bm1 = fmaxf(s4[1], s4[3]);
+                    if (__any_sync(0xffffffffu, bm0 > m[0] + kLazy || bm1 > m[1] + kLazy)) {
+                        float r0 = bm0, r1 = bm1;
 #pragma unroll
-                        for (int msk = LPT; msk < 32; msk <<= 1)
-                            bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, msk));
-                        const float mn = fmaxf(m, bm);
-                        const float alpha = ptx::ex2(m - mn);
-                        m = mn;
-                        l *= alpha;
-                        if (head_writer && tg == 0) alph[hsel] = alpha;
-                        __syncwarp();
+                        for (int msk = 4; msk < 32; msk <<= 1) {
+                            r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, msk));
+                            r1 = fmaxf(r1, __shfl_xor_sync(0xffffffffu, r1, msk));
+                        }
+                        const float n0 = fmaxf(m[0], r0), n1 = fmaxf(m[1], r1);
+                        const float al0 = n0 == -INFINITY ? 1.f : ptx::ex2(m[0] - n0);
+                        const float al1 = n1 == -INFINITY ? 1.f : ptx::ex2(m[1] - n1);
+                        m[0] = n0;
+                        m[1] = n1;
+                        l[0] *= al0;
+                        l[1] *= al1;
 #pragma unroll
-                        for (int h = 0; h < G; ++h) {
-                            const float al = alph[h];
-#pragma unroll
-                            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::fmul2(o2[h][i], make_float2(al, al));
+                        for (int t = 0; t < KS; ++t) {
+                            o[t][0] *= al0;
+                            o[t][2] *= al0;
+                            o[t][1] *= al1;
+                            o[t][3] *= al1;
                         }
                     }
+                    float p[4];
 #pragma unroll
-                    for (int it = 0; it < NIT; ++it) {
-                        s[it] = ptx::ex2(s[it] - m);
-                        l += s[it];
+                    for (int i = 0; i < 4; ++i) {
+                        const float mm = m[i & 1];
+                        p[i] = mm == -INFINITY ? 0.f : ptx::ex2(s4[i] - mm);
                     }
-                    if (head_writer) {
-#pragma unroll
-                        for (int it = 0; it < NIT; ++it) ps[(it * TPI + tg) * G + hsel] = s[it];
+                    l[0] += p[0] + p[2];
+                    l[1] += p[1] + p[3];
+                    // ---- P^T as the B operand of P.V: lane (g, c) needs p(token 2c, 2c+1 | +8,
+                    // head g), held by lanes 8c + g/2 (+4) -> 8 shuffles, then an exact bf16
+                    // hi + lo split (P carries ~16 bits into the fp32 accumulation) ----
+                    const bool odd = g & 1;
+                    float q0, q1, q2, q3;
+                    {
+                        const float x0 = __shfl_sync(0xffffffffu, p[0], e_src), x1 = __shfl_sync(0xffffffffu, p[1], e_src);
+                        const float y0 = __shfl_sync(0xffffffffu, p[0], e_src + 4), y1 = __shfl_sync(0xffffffffu, p[1], e_src + 4);
+                        const float z0 = __shfl_sync(0xffffffffu, p[2], e_src), z1 = __shfl_sync(0xffffffffu, p[3], e_src);
+                        const float w0 = __shfl_sync(0xffffffffu, p[2], e_src + 4), w1 = __shfl_sync(0xffffffffu, p[3], e_src + 4);
+                        q0 = odd ? x1 : x0;   // p(2c, g)
+                        q1 = odd ? y1 : y0;   // p(2c+1, g)
+                        q2 = odd ? z1 : z0;   // p(2c+8, g)
+                        q3 = odd ? w1 : w0;   // p(2c+9, g)
                     }
-                    __syncwarp();
-                    // ---- o += P.V: lane owns dims [lane*DPL, +DPL) of all G heads ----
-                    auto pv_token = [&](int t) {
-                        float p[G];
-                        if constexpr (G % 4 == 0) {
+                    const uint32_t bh0 = ptx::f2_to_bf2(q0, q1), bh1 = ptx::f2_to_bf2(q2, q3);
+                    const float2 r01 = ptx::bf2_to_f2(bh0), r23 = ptx::bf2_to_f2(bh1);
+                    const uint32_t bl0 = ptx::f2_to_bf2(q0 - r01.x, q1 - r01.y);
+                    const uint32_t bl1 = ptx::f2_to_bf2(q2 - r23.x, q3 - r23.y);
+                    // ---- O^T (d x 8 heads) += V^T . P^T ----
 #pragma unroll
-                            for (int h4 = 0; h4 < G; h4 += 4) {
-                                const float4 p4 = *reinterpret_cast<const float4 *>(ps + t * G + h4);
-                                p[h4] = p4.x; p[h4 + 1] = p4.y; p[h4 + 2] = p4.z; p[h4 + 3] = p4.w;
-                            }
-                        } else if constexpr (G == 2) {
-                            const float2 p2 = *reinterpret_cast<const float2 *>(ps + t * 2);
-                            p[0] = p2.x; p[1] = p2.y;
-                        } else {
-                            p[0] = ps[t];
-                        }
-                        float2 v[NP];
-                        if constexpr (NP == 2) {
-                            const uint2 raw = *reinterpret_cast<const uint2 *>(vb + t * (D * 2) + lane * 8);
-                            v[0] = ptx::bf2_to_f2(raw.x);
-                            v[1] = ptx::bf2_to_f2(raw.y);
-                        } else {
-                            v[0] = ptx::bf2_to_f2(*reinterpret_cast<const uint32_t *>(vb + t * (D * 2) + lane * 4));
-                        }
-#pragma unroll
-                        for (int h = 0; h < G; ++h)
-#pragma unroll
-                            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(p[h], p[h]), v[i], o2[h][i]);
-                    };
-                    if (ntok == kBlockTok) {
-#pragma unroll
-                        for (int t = 0; t < kBlockTok; ++t) pv_token(t);
-                    } else {
-                        for (int t = 0; t < ntok; ++t) pv_token(t);
+                    for (int t = 0; t < KS; ++t) {
+                        uint32_t a0, a1, a2, a3;
+                        ptx::ldsm_x4_t(vb + swz(v_tok, 16 * t + v_d), a0, a1, a2, a3);
+                        ptx::mma_16816(o[t], a0, a1, a2, a3, bh0, bh1);
+                        ptx::mma_16816(o[t], a0, a1, a2, a3, bl0, bl1);
                     }
                     __syncwarp();
                     ++c_count;
@@ -509,29 +593,49 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 fill();
             }
 
-            // ---- combine l over the TPI token groups (o is already per dim) ----
+            // ---- the unit's per-head sums over the 8 lanes of each head pair ----
 #pragma unroll
-            for (int msk = LPT; msk < 32; msk <<= 1) l += __shfl_xor_sync(0xffffffffu, l, msk);
-            // per-head (m, l) from the lane that owns each head
-            float mh[G], lh[G];
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                mh[h] = __shfl_sync(0xffffffffu, m, h * (LPT / G));
-                lh[h] = __shfl_sync(0xffffffffu, l, h * (LPT / G));
+            for (int msk = 4; msk < 32; msk <<= 1) {
+                l[0] += __shfl_xor_sync(0xffffffffu, l[0], msk);
+                l[1] += __shfl_xor_sync(0xffffffffu, l[1], msk);
             }
             const int nslots = m1.x, nseg = m1.y;
-            // first global write of this grid: the previous kernel(s) must be complete
-            wait_k1();
             if (nseg == 1) {
-                finalize<D, G>(a, req, head, nslots, lane, mh, lh, o2, lse0, have0);
+                if (k1_hint()) {
+                    wait_k1();  // first output write of this grid: K1 (and before it the previous K2) done
+                    finalize<D, G>(a, req, head, nslots, lane, m, l, o, lse0, have0);
+                } else {
+                    // K1 still runs: park the unit's state (L2) and stream on; merged by drain()
+                    float *pk = park + (int64_t)u * PARK_UNIT;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int h = 2 * c + e;
+                        if (h >= G) continue;
+#pragma unroll
+                        for (int t = 0; t < KS; ++t) {
+                            pk[h * D + 16 * t + g] = o[t][e];
+                            pk[h * D + 16 * t + g + 8] = o[t][2 + e];
+                        }
+                        if (g == 0) *reinterpret_cast<float2 *>(pk + G * D + 2 * h) = make_float2(m[e], l[e]);
+                    }
+                    if (lane == 0) plist[npark] = u;
+                    ++npark;
+                    if (npark == NPARK) drain();
+                }
             } else {
                 // ---- stream-K: publish this piece's state; the last piece merges them all ----
                 const int slot = m1.z + (cc - m1.w);
+                float *so = seg_o + (int64_t)slot * (NPAD * D) + lane * (4 * KS);
+                if (2 * c < G) {
 #pragma unroll
-                for (int h = 0; h < G; ++h) st_pairs<NP>(P.seg_o + ((int64_t)slot * G + h) * D + lane * DPL, o2[h], 1.f);
+                    for (int t = 0; t < KS; ++t) *reinterpret_cast<float4 *>(so + 4 * t) = make_float4(o[t][0], o[t][1], o[t][2], o[t][3]);
+                }
+                if (g == 0) {
 #pragma unroll
-                for (int h = 0; h < G; ++h)
-                    if (lane == h) *reinterpret_cast<float2 *>(P.seg_ml + ((int64_t)slot * G + h) * 2) = make_float2(mh[h], lh[h]);
+                    for (int e = 0; e < 2; ++e)
+                        if (2 * c + e < G)
+                            *reinterpret_cast<float2 *>(seg_ml + ((int64_t)slot * NPAD + 2 * c + e) * 2) = make_float2(m[e], l[e]);
+                }
                 // one acq_rel arrival by lane 0: release covers the whole warp's stores
                 // (ordered before it by the warp barrier), acquire makes the other pieces'
                 // stores visible to the merging warp (read from L2 with ld.cg)
@@ -539,58 +643,40 @@ __global__ void __launch_bounds__(kWarps * 32, 1) suffix_decode_kernel(const Suf
                 int old = 0;
                 if (lane == 0)
                     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                                 : "=r"(old) : "l"(P.unit_count + u) : "memory");
+                                 : "=r"(old) : "l"(unit_count + u) : "memory");
                 old = __shfl_sync(0xffffffffu, old, 0);
                 if (old == nseg - 1) {
-                    if (lane == 0) P.unit_count[u] = 0;  // ready for the next launch
-                    // merge all pieces in segment order (deterministic), from L2; the first
-                    // K1 partial lse is requested up front so its latency overlaps the merge
-                    float lseM[G];
-                    const bool haveM = nslots > 0;
-                    {
-                        const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
-#pragma unroll
-                        for (int h = 0; h < G; ++h) lseM[h] = haveM ? __ldcg(src + h) : 0.f;
+                    if (lane == 0) unit_count[u] = 0;  // ready for this slot's next launch
+                    if (k1_hint()) {
+                        wait_k1();
+                        merge_pieces(u);
+                    } else {
+                        if (lane == 0) plist[npark] = u | (int)0x80000000;
+                        ++npark;
+                        if (npark == NPARK) drain();
                     }
-                    float M[G], L[G];
-#pragma unroll
-                    for (int h = 0; h < G; ++h) { M[h] = -INFINITY; L[h] = 0.f; }
-                    const int base = m1.z;
-                    for (int sg = 0; sg < nseg; ++sg)
-#pragma unroll
-                        for (int h = 0; h < G; ++h)
-                            M[h] = fmaxf(M[h], __ldcg(P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
-#pragma unroll
-                    for (int h = 0; h < G; ++h)
-#pragma unroll
-                        for (int i = 0; i < NP; ++i) o2[h][i] = make_float2(0.f, 0.f);
-                    for (int sg = 0; sg < nseg; ++sg) {
-#pragma unroll
-                        for (int h = 0; h < G; ++h) {
-                            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(
-                                P.seg_ml + ((int64_t)(base + sg) * G + h) * 2));
-                            const float w = (ml.y > 0.f) ? ptx::ex2(ml.x - M[h]) : 0.f;
-                            L[h] += ml.y * w;
-                            float2 x[NP];
-                            ld_pairs_cg<NP>(P.seg_o + ((int64_t)(base + sg) * G + h) * D + lane * DPL, x);
-#pragma unroll
-                            for (int i = 0; i < NP; ++i) o2[h][i] = ptx::ffma2(make_float2(w, w), x[i], o2[h][i]);
-                        }
-                    }
-                    finalize<D, G>(a, req, head, nslots, lane, M, L, o2, lseM, haveM);
-
                 }
             }
             __syncwarp();
+        }
+    }
+    if (npark > 0) drain();
+    // the launch's last warp resets this layer slot's completion hints
+    __syncwarp();
+    if (lane == 0) {
+        const uint32_t done = atomicAdd(P.k2_done + ls, 1u);
+        if (done == (uint32_t)P.nwarps - 1) {
+            P.k1_done[ls] = 0;
+            P.k2_done[ls] = 0;
         }
     }
     K2_TRACE(gw, 3);
 }
 
 template <int D, int G, int kWarps, int kStages>
-cudaError_t launch_t(const SuffixArgs &a, cudaStream_t s) {
+cudaError_t launch_t(const CUtensorMap *tmk, const CUtensorMap *tmv, const SuffixArgs &a, cudaStream_t s) {
     using S = Shape<D, G, kWarps, kStages>;
-    const int smem = kWarps * S::WARP_SMEM_AL;
+    const int smem = S::SMEM;
     auto kern = suffix_decode_kernel<D, G, kWarps, kStages>;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -613,31 +699,29 @@ cudaError_t launch_t(const SuffixArgs &a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.p.ntiles > 0 ? 1 : 0;  // overlap K1 only (never a previous K2)
-    return cudaLaunchKernelEx(&cfg, kern, a);
+    return cudaLaunchKernelEx(&cfg, kern, *tmk, *tmv, a);
 }
 
 }  // namespace
 
-cudaError_t launch_suffix_decode(const PlanDev &p, const PoolGeom &g, const void *pool_k,
-                                 const void *pool_v, int layer, const void *q, float *out,
-                                 float *lse, float scale, int num_sms, cudaStream_t s) {
-    (void)num_sms;  // the grid follows the plan's warp count
+cudaError_t launch_suffix_decode(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v, const PlanDev &p,
+                                 const PoolGeom &g, int layer, const void *q, float *out, float *lse,
+                                 float scale, cudaStream_t s) {
     SuffixArgs a;
     a.p = p;
-    a.pool_k = static_cast<const uint16_t *>(pool_k);
-    a.pool_v = static_cast<const uint16_t *>(pool_v);
-    a.layer_off = (int64_t)layer * g.cap * g.hkv * kBlockTok * g.d;
+    a.layer_blk = (int64_t)layer * g.cap;
     a.q = static_cast<const uint16_t *>(q);
     a.out = out;
     a.lse = lse;
     a.hkv = g.hkv;
     a.hq = g.hq;
     a.qscale = scale * kLog2e;
+    a.layer = layer;
     const int G = g.hq / g.hkv;
 #define HALO_K2_CASE(DD, GG)                                                                       \
     if (g.d == DD && G == GG)                                                                      \
-        return p.k2_warps == kK2WarpsNarrow ? launch_t<DD, GG, kK2WarpsNarrow, kK2StagesNarrow>(a, s) \
-                                            : launch_t<DD, GG, kK2WarpsWide, kK2StagesWide>(a, s);
+        return p.k2_warps == kK2WarpsNarrow ? launch_t<DD, GG, kK2WarpsNarrow, kK2StagesNarrow>(tmap_k, tmap_v, a, s) \
+                                            : launch_t<DD, GG, kK2WarpsWide, kK2StagesWide>(tmap_k, tmap_v, a, s);
     HALO_K2_CASE(128, 1) HALO_K2_CASE(128, 2) HALO_K2_CASE(128, 4) HALO_K2_CASE(128, 8)
     HALO_K2_CASE(64, 1) HALO_K2_CASE(64, 2) HALO_K2_CASE(64, 4) HALO_K2_CASE(64, 8)
 #undef HALO_K2_CASE

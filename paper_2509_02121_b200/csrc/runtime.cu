@@ -852,7 +852,31 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             if (!bal) cuts = equal_cuts(Ww, kK2WarpsWide);  // equal item ranges (stream-K pieces)
         }
         if (cuts.size() < 2) cuts = {0, Itot};
+        // static-then-dynamic: the wide shape's stream-K cuts get a dynamic tail -- the warps'
+        // static shares cover the first (100 - tail)% of the items, the rest is cut into
+        // pieces of about `piece` items that warps claim once their share is done
+        pl->dyn_first = (int32_t)cuts.size() - 1;
+        {
+            const int tail_pct = std::max(0, pl->opt.k2_tail_pct);  // off by default (A/B: tools/k2_tail_ab.sh)
+            const int64_t W = (int64_t)k2_sms(pl) * pl->k2_warps;
+            const bool eligible = tail_pct > 0 && pl->opt.k2_chunk_blocks <= 0 && pl->k2_warps == kK2WarpsWide &&
+                                  !bal && Itot >= 8 * W;
+            if (eligible) {
+                const int64_t front = Itot - Itot * std::min(tail_pct, 50) / 100;
+                std::vector<int64_t> c(1, 0);
+                for (int64_t w = 1; w < W; ++w) push_cut(c, target(w, W, pl->k2_warps) * front / Itot);
+                push_cut(c, front);
+                if ((int64_t)c.size() - 1 == W) {  // exactly one static chunk per warp
+                    const int64_t piece = std::max<int64_t>(2, (Itot - front) / (2 * W));
+                    for (int64_t x = front + piece; x < Itot; x += piece) push_cut(c, x);
+                    c.push_back(Itot);
+                    cuts.swap(c);
+                    pl->dyn_first = (int32_t)W;
+                }
+            }
+        }
         const int64_t nchunks = (int64_t)cuts.size() - 1;
+        if (pl->dyn_first > nchunks) pl->dyn_first = (int32_t)nchunks;
         auto block_at = [&](int64_t x) {  // global block index where item x starts
             if (x >= Itot) return Btot;
             const int64_t u = unit_of(x);
@@ -1009,8 +1033,13 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
         HALO_CUDA(cudaMalloc(&pl->part, cap * 4));
         pl->part_cap = cap;
     }
-    const size_t seg_elems = (size_t)pl->nseg_total * (p->cfg.num_q_heads / p->cfg.num_kv_heads) *
-                             (p->cfg.head_dim + 2);
+    // K2 scratch, four layer slots (a K2 launch may overlap the previous layer's): stream-K
+    // pieces (o in K2's fragment layout, kK2HeadPad heads x d, + (m, l) per head) and parked
+    // whole-unit states (g heads x (d + 2)) -- one buffer
+    const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
+    const size_t seg_slot = (size_t)std::max(pl->nseg_total, 1) * kK2HeadPad * (p->cfg.head_dim + 2);
+    const size_t park_slot = (size_t)U * gq * (p->cfg.head_dim + 2);
+    const size_t seg_elems = 4 * (seg_slot + park_slot);
     if (pl->seg_cap < seg_elems) {
         if (pl->segbuf) {
             HALO_CUDA(cudaStreamSynchronize(s));
@@ -1021,17 +1050,19 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
         HALO_CUDA(cudaMalloc(&pl->segbuf, cap * 4));
         pl->seg_cap = cap;
     }
-    if (pl->counter_cap < (size_t)U + 2) {
+    // counters: unit arrivals x 4 slots, then dyn claims [4], K1 done [4], K2 done [4]
+    const size_t ncount = 4 * ((size_t)U + 2) + 12;
+    if (pl->counter_cap < ncount) {
         if (pl->counters) {
             HALO_CUDA(cudaStreamSynchronize(s));
             cudaFree(pl->counters);
             pl->counters = nullptr;
         }
-        const size_t cap = U + U / 4 + 64;
+        const size_t cap = ncount + U + 64;
         HALO_CUDA(cudaMalloc(&pl->counters, cap * 4));
         pl->counter_cap = cap;
     }
-    HALO_CUDA(cudaMemsetAsync(pl->counters, 0, ((size_t)U + 2) * 4, s));
+    HALO_CUDA(cudaMemsetAsync(pl->counters, 0, ncount * 4, s));
     HALO_CUDA(pl->pin_plan.commit(pl->dbuf, total, s));
     uint8_t *d = static_cast<uint8_t *>(pl->dbuf);
     PlanDev &dv = pl->dev;
@@ -1052,15 +1083,21 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     dv.unit_nseg = reinterpret_cast<const int32_t *>(d + o_unseg);
     dv.unit_seg = reinterpret_cast<const int32_t *>(d + o_useg);
     dv.unit_count = pl->counters;
+    dv.count_slot_stride = U + 2;
+    dv.dyn_counter = pl->counters + 4 * (U + 2);
+    dv.k1_done = reinterpret_cast<uint32_t *>(pl->counters + 4 * (U + 2) + 4);
+    dv.k2_done = reinterpret_cast<uint32_t *>(pl->counters + 4 * (U + 2) + 8);
+    dv.dyn_first = pl->dyn_first;
     dv.k2_ent = reinterpret_cast<const uint2 *>(d + o_ent);
     dv.unit_meta = reinterpret_cast<const int4 *>(d + o_umeta);
     dv.chunk_info = reinterpret_cast<const int4 *>(d + o_cinfo);
     dv.tile_aux = reinterpret_cast<const int4 *>(d + o_taux);
     dv.nchunks = NC;
     dv.nblocks = pl->unit_boff.empty() ? 0 : pl->unit_boff.back();
-    const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
     dv.seg_o = pl->segbuf;
-    dv.seg_ml = pl->segbuf + (size_t)pl->nseg_total * gq * p->cfg.head_dim;
+    dv.seg_ml = pl->segbuf + (size_t)std::max(pl->nseg_total, 1) * kK2HeadPad * p->cfg.head_dim;
+    dv.seg_slot_stride = (int64_t)seg_slot;
+    dv.park = pl->segbuf + 4 * seg_slot;
     dv.nwarps = k2_sms(pl) * pl->k2_warps;
     dv.k2_warps = pl->k2_warps;
     dv.ntiles = (int32_t)pl->tiles.size();
@@ -1091,7 +1128,7 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
         if (e != cudaSuccess) return fail(HALO_ECUDA, "prefix kernel launch: %s", cudaGetErrorString(e));
     }
     if (mask & 2) {
-        e = launch_suffix_decode(pl->dev, p->geom, p->k, p->v, layer, q, out, lse, scale, p->num_sms, s);
+        e = launch_suffix_decode(&p->tmap_k, &p->tmap_v, pl->dev, p->geom, layer, q, out, lse, scale, s);
         if (e != cudaSuccess) return fail(HALO_ECUDA, "suffix kernel launch: %s", cudaGetErrorString(e));
     }
     return HALO_OK;

@@ -142,6 +142,7 @@ struct halo_plan_s {
     std::vector<int32_t> req_order, node_blocks, unit_req, req_blk_off, req_nslots;
     std::vector<int32_t> unit_boff, chunk_lo, chunk_u0, chunk_u1, unit_chunk0, unit_nseg, unit_seg;
     int32_t nseg_total = 0;
+    int32_t dyn_first = 0;  // first dynamically claimed K2 chunk (== nchunks: none)
     int32_t k2_warps = halo::kK2WarpsWide;
     bool k2_early = false;  // K1 split count lowered so K2's first CTAs stream beside K1
     std::vector<uint32_t> req_blk;

@@ -37,7 +37,11 @@ def main():
     wl = make_config(cfg, layers=int(os.environ.get("LAYERS", "2")))
     ld = load(wl, 0)
     append_step(ld, wl, 0, 0)
-    plan = ld.pool.plan(ld.req_ids)
+    from paper_2509_02121_b200.abi import PlanOptions
+    opt = PlanOptions(0, 0, int(os.environ.get("SPLITS", "0")), 0)
+    opt.k2_early_weight = float(os.environ.get("EARLY_W", "0"))
+    opt.k1_sm_frac = float(os.environ.get("K1_SM_FRAC", "0"))
+    plan = ld.pool.plan(ld.req_ids, opt)
     info = plan.info()
     q = wl.q(0, "cuda:0")
     out = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda:0")
@@ -72,7 +76,13 @@ def main():
         ncta_warps = int(os.environ.get("K2_WARPS", "0")) or None
         if ncta_warps:
             ends = t[:, 3][: (len(t) // ncta_warps) * ncta_warps].reshape(-1, ncta_warps).max(axis=1)
+            starts = t[:, 0][: (len(t) // ncta_warps) * ncta_warps].reshape(-1, ncta_warps).min(axis=1)
             print("per-CTA exit: min %.2f median %.2f max %.2f" % (ends.min(), np.median(ends), ends.max()))
+            early = starts < 2.0
+            for name, sel in (("early CTAs", early), ("late CTAs", ~early)):
+                if sel.any():
+                    print(f"  {name:10s} n={sel.sum():3d} start p50 {np.median(starts[sel]):6.2f} "
+                          f"exit min {ends[sel].min():6.2f} p50 {np.median(ends[sel]):6.2f} max {ends[sel].max():6.2f}")
     plan.destroy()
     ld.pool.destroy()
 

@@ -398,10 +398,10 @@ int k2_sms(halo_plan pl) {
     const int n = pl->opt.k2_sms, all = pl->pool->num_sms;
     return (n > 0 && n < all) ? n : all;
 }
-double k2_early_weight(halo_plan pl) { return pl->opt.k2_early_weight > 0 ? pl->opt.k2_early_weight : 1.2; }
+double k2_early_weight(halo_plan pl) { return pl->opt.k2_early_weight > 0 ? pl->opt.k2_early_weight : pl->k2_early_w; }
 double k1_sm_frac(halo_plan pl) {
     const float f = pl->opt.k1_sm_frac;
-    return f < 0 ? 0.0 : f == 0 ? 0.65 : (double)f;
+    return f < 0 ? 0.0 : f == 0 ? 0.75 : (double)f;
 }
 
 // `virt` (prefill): the plan's rows are these virtual requests -- one per new prompt token,
@@ -538,16 +538,24 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         }
     } else {
         int C = choose_chunk(ns, g, hkv, p->num_sms, max_splits);
-        // K1 in a single partial wave beside a K2 that dominates the layer: under programmatic
-        // dependent launch K2's first CTAs stream on the SMs K1 leaves idle, so fewer, longer
-        // K1 tiles (split count lowered until the tiles fit k1_sm_frac of the SMs) free SMs
-        // for K2 while K1 runs; K2's early CTAs then get a larger share (section 12b).  Applied
-        // only when K2's estimated time is at least 2.4x K1's at the lowered split count: below
-        // that, K2's early units wait for K1 at their merge (measured on 8 fan-out shapes,
-        // tools/k2_early_sweep3.sh: ratios 2.5-10 gain 3-8%, ratios ~2.1 lose 4-11%).
-        // (C1: 4 -> 3 splits, 128 -> 96 K1 CTAs, 3.59 -> 3.71 M queries/s; K2.)
+        // K1 in a single partial wave beside a K2 that dominates the layer (co-schedule model).
+        // Under programmatic dependent launch K2's first (SMs - K1 CTAs) CTAs stream on the SMs
+        // K1 leaves idle; K2 parks finished units until K1 is done.  For each split count whose
+        // tiles fit one wave the model estimates
+        //   T1 = t0 + t_n * (n-tiles per K1 CTA)                  (K1 CTA duration)
+        //   early = E * r_e * T1                                  (E = SMs - K1 CTAs)
+        //   T  = T1 + max(0, B - early) / R                       (B = K2 bytes, R = HBM)
+        // and takes the split count of least T (if it beats the default tiling).  K2's early CTAs
+        // get w = (r_e T1 + r_pe T2) / (r_pl T2) times a late CTA's share (T2 = T - T1; CTAs
+        // already streaming keep more of the bandwidth after K1 than the ones entering then).
+        // Constants measured on B200 (round 2: tools/k1k2_cosched_sweep.py, tools/k2_trace.py,
+        // profiles/k1k2_cosched_r02b.txt, k2_trace_cosched_r02.txt).
         pl->k2_early = false;
+        pl->k2_early_w = 1.0;
         if (k1_sm_frac(pl) > 0 && pl->opt.max_splits <= 0) {
+            constexpr double kT0 = 3.0, kTn = 2.75;          // us: K1 CTA prologue+epilogue, per n-tile
+            constexpr double kRe = 44e3, kRpe = 56e3, kRpl = 23e3;  // bytes/us per SM: beside K1, after K1
+            constexpr double kR = 6.2e6;                     // bytes/us: HBM, K2 streaming on all SMs
             auto tiles_for = [&](int64_t Cc, int64_t &max_ch) {
                 int64_t T = 0;
                 max_ch = 0;
@@ -562,22 +570,46 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
                 }
                 return T;
             };
+            double B = 0;
+            for (int i = 0; i < nreq; ++i) B += (double)R[i]->blocks.size() * kBlockTok * hkv * D * 4;
+            const int sms = k2_sms(pl);
+            auto model = [&](int64_t tiles, int64_t max_ch, double &w) {
+                const double t1 = kT0 + kTn * (double)ceil_div(max_ch, kK1Tok);
+                const int64_t waves = ceil_div(tiles, (int64_t)sms);
+                if (waves > 1) {  // multi-wave K1: K2 streams beside its last wave only (ignored)
+                    w = 1.0;
+                    return (double)waves * t1 + B / kR;
+                }
+                const double E = (double)(sms - tiles), re = std::min(kRe, kR / std::max(E, 1.0));
+                const double rest = std::max(0.0, B - E * re * t1);
+                const double t2 = rest / kR;
+                w = t2 > 0 ? std::min(8.0, std::max(1.0, (re * t1 + kRpe * t2) / (kRpl * t2))) : 8.0;
+                return t1 + t2;
+            };
             int64_t mc = 0;
-            const int64_t T0 = tiles_for(C, mc);
-            double k2_bytes_est = 0;
-            for (int i = 0; i < nreq; ++i) k2_bytes_est += (double)R[i]->blocks.size() * kBlockTok * hkv * D * 4;
-            const double cap = k1_sm_frac(pl) * p->num_sms;
-            if (T0 > 0 && T0 <= p->num_sms && (double)T0 > cap) {
-                for (int64_t Cc = C + kK1Tok; Cc <= kK1MaxTileTok; Cc += kK1Tok) {
-                    const int64_t T1 = tiles_for(Cc, mc);
-                    if ((double)T1 > cap) continue;
-                    const double t_k1_us = 3.5 + 2.4 * (double)ceil_div(mc, kK1Tok);  // measured per-CTA
-                    const double t_k2_us = k2_bytes_est / 6.0e6;                       // ~6 TB/s
-                    if (T1 > 0 && t_k2_us >= 2.4 * t_k1_us) {
-                        C = (int)Cc;
-                        pl->k2_early = true;
-                    }
-                    break;
+            double w0 = 1.0;
+            const int64_t tiles0 = tiles_for(C, mc);  // (sets mc: not inside the call's arguments)
+            const double base = model(tiles0, mc, w0);
+            double best = base * 0.98;  // switch only for a clear gain
+            // only when K2 dominates the layer: its HBM time >= 1.25x the default K1 CTA time,
+            // and >= 8 blocks per K2 warp (with fewer, K2 is bound by per-unit latency, which the
+            // model does not capture: 64 x 8192-token fan-out lost 13% with the rule)
+            const double t1_base = kT0 + kTn * (double)ceil_div(mc, kK1Tok);
+            const double blocks_per_warp = B / ((double)kBlockTok * hkv * D * 4) * hkv / ((double)sms * kK2WarpsWide);
+            if (B / kR < 1.25 * t1_base || blocks_per_warp < 8.0) best = 0;
+            for (int64_t Cc = kK1Tok; Cc <= kK1MaxTileTok && best > 0; Cc += kK1Tok) {
+                const int64_t T1 = tiles_for(Cc, mc);
+                // K1 on 40..k1_sm_frac of the SMs: with fewer K1 CTAs (longer tiles) the measured
+                // layer time departs from the model (C1, 32 CTAs: 75 us measured vs 54 modeled)
+                if (T1 <= 0 || T1 > (int64_t)(k1_sm_frac(pl) * sms) || T1 >= sms || T1 < (int64_t)(0.4 * sms))
+                    continue;
+                double w = 1.0;
+                const double t = model(T1, mc, w);
+                if (t < best) {
+                    best = t;
+                    C = (int)Cc;
+                    pl->k2_early = true;
+                    pl->k2_early_w = w;
                 }
             }
         }

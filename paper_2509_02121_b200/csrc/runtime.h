@@ -145,6 +145,7 @@ struct halo_plan_s {
     int32_t dyn_first = 0;  // first dynamically claimed K2 chunk (== nchunks: none)
     int32_t k2_warps = halo::kK2WarpsWide;
     bool k2_early = false;  // K1 split count lowered so K2's first CTAs stream beside K1
+    double k2_early_w = 1.0;  // the co-schedule model's work weight of those CTAs
     std::vector<uint32_t> req_blk;
     std::vector<uint32_t> k2_ent;     // [Btot][2] K2 block descriptors (PlanDev::k2_ent)
     std::vector<int32_t> unit_meta;   // [U][8] K2 unit metadata (PlanDev::unit_meta)

@@ -371,9 +371,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-migration", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
-    ap.add_argument("--other-configs", default="tree,analytics",
+    ap.add_argument("--other-configs", default="tree,tree_root,tree_roles,analytics",
                     help="BASELINE configs also measured per launch (C2 tree, C3 analytics); '' = none")
     ap.add_argument("--other-layers", type=int, default=4)
+    ap.add_argument("--strong-layers", type=int, default=32, help="layers of the C2 strong-scaling leg")
     ap.add_argument("--layers", type=int, default=0, help="override the config's layer count (profiling)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: debug the N>1 path with several ranks on one GPU")
@@ -435,6 +436,45 @@ def main():
         traffic = json.load(open(tp)).get("suffix_decode_kernel", {}).get("dram_bytes_per_launch")
 
     extra = {}
+
+    def guarded(key, fn):
+        """The secondary legs must not cost the headline line: a failure is reported in place."""
+        try:
+            extra[key] = fn()
+        except Exception as e:  # noqa: BLE001
+            extra[key] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.synchronize()
+    # ---- K2 with equal per-warp shares (the co-schedule weights off, same K1 splits): the
+    # kernel's own capability; the breakdown pass above runs K2 alone with the weights the
+    # planner set for running BESIDE K1, which leaves it imbalanced by design ----
+    if not args.profile:
+        def k2_equal():
+            eopt = halo.PlanOptions(0, 0, int(os.environ.get("HALO_MAX_SPLITS", "0")), 0)
+            eopt.k2_early_weight = 1.0
+            ep = pool.plan(reqs, eopt)
+            einfo = ep.info()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+            for rep in range(4):
+                for l in range(L):
+                    ep.run_stages(l, 1, q[l], out[l], lse[l])
+                    if rep == 3:
+                        evs[l][0].record(stream)
+                    ep.run_stages(l, 2, q[l], out[l], lse[l])
+                    if rep == 3:
+                        evs[l][1].record(stream)
+            torch.cuda.synchronize()
+            k2ms = sum(a.elapsed_time(b) for a, b in evs) / L
+            ep.destroy()
+            r = kernel_rooflines(einfo, k1_launch_ms, k2ms)[0]
+            r["timing"] = "CUDA events around each K2 launch (K1 before it, serialised), 32 layers"
+            return r
+        guarded("roofline_k2_equal_shares", k2_equal)
+        hbm_peak = peaks()[0]
+        lay_bytes = info["k2_bytes"] + info["k1_bytes"]
+        lay_ms = ms_step / L
+        extra["layer_roofline"] = {"bound": "hbm", "what": "K1 + K2 algorithmic bytes per layer / headline "
+                                   "time per layer (the kernels overlap under PDL)", "achieved": lay_bytes / lay_ms / 1e6,
+                                   "peak": hbm_peak, "unit": "GB/s", "frac": lay_bytes / lay_ms / 1e6 / hbm_peak}
     # ---- e2e: the public API with HOST buffers (pinned), copies inside the timed region ----
     if not args.no_e2e and not args.profile:
         nk_h, nv_h = nk.cpu().pin_memory(), nv.cpu().pin_memory()
@@ -465,13 +505,6 @@ def main():
                         "plan + all layers; H2D in 4-layer and D2H in 2-layer chunks on library "
                         "copy streams, overlapped with the kernels) with pinned host buffers; "
                         "wall clock after sync"}
-    def guarded(key, fn):
-        """The secondary legs must not cost the headline line: a failure is reported in place."""
-        try:
-            extra[key] = fn()
-        except Exception as e:  # noqa: BLE001
-            extra[key] = {"error": f"{type(e).__name__}: {e}"}
-            torch.cuda.synchronize()
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
         guarded("migration", lambda: measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist,
@@ -496,7 +529,7 @@ def main():
     # ---- strong scaling: C2 with its kv heads sharded over the ranks ----
     if args.other_configs and not args.profile:
         guarded("strong_scaling", lambda: measure_strong_scaling(
-            halo, args.other_layers, max(3, min(args.steps, 10)), 3, world, rank, dev, torch, dist))
+            halo, args.strong_layers, max(3, min(args.steps, 10)), 3, world, rank, dev, torch, dist))
     # ---- CPU oracle baseline ----
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         n, t, cores = oracle_sample(wl, args.cpu_budget)

@@ -288,7 +288,23 @@ def scaled(seed=6, layers=2, hq=8, hkv=2, d=128, dist="normal", **kw):
     return Workload("scaled", layers, hq, hkv, d, nodes, reqs, seed, dist=dist, **kw)
 
 
+def tree_root(seed=2, layers=32, **kw):
+    """C2's root node class alone: 1024 requests under one 4096-token prefix (K1 rows 4096 per
+    kv head, arithmetic intensity 4096) -- the C2-root K1 gate of SURVEY.md §8(d)."""
+    return _fanout("tree_root", layers, 32, 8, 128, 1024, 4096, 255, seed, **kw)
+
+
+def tree_roles(seed=2, layers=32, **kw):
+    """C2's role node class alone: 16 prefixes of 1024 tokens with 64 requests each (K1 rows
+    256 per kv head, arithmetic intensity 256 ~ the ridge)."""
+    nodes = [NodeSpec(i, -1, 1024) for i in range(16)]
+    reqs = [RequestSpec(i, i // 64, 255) for i in range(1024)]
+    return Workload("tree_roles", layers, 32, 8, 128, nodes, reqs, seed, **kw)
+
+
 CONFIGS = {
+    "tree_root": tree_root,
+    "tree_roles": tree_roles,
     "scaled": scaled,
     "toy": toy,
     "fanout": fanout,

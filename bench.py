@@ -318,6 +318,114 @@ def measure_other_configs(halo, names, layers, steps, warmup, world, dev, torch,
     return res
 
 
+def measure_placed_c3(halo, layers, steps, warmup, world, rank, dev, torch, dist, link_gbs, nccl_ok):
+    """BASELINE configs[3] (C3 batch analytics: 64 templates x 8k-token contexts, 256 requests
+    each, over 8 GPUs "with cross-GPU prefix placement") at this N: 8 templates per GPU.  Each
+    template's KV starts on GPU t % N (prefilled where it arrived); the relocation planner
+    (halo_place_groups, Alg. 1 with the §3.2 costs) places the templates over the
+    GPUs; the moves run through halo_migrate_exchange (NCCL) before the timed steps; then every
+    GPU decodes the requests of the templates it holds (no exchange on the attention path).
+    Aggregate queries/s = all requests x layers / max-over-ranks time."""
+    from paper_2509_02121_b200.loader import blocks_needed
+    from paper_2509_02121_b200.relocation import plan_relocation, rank_actions
+    from synth import make_config
+    T = 8 * world
+    wl = make_config("analytics", templates=T, layers=layers)
+    hbm, tc = peaks()[:2]
+    homes = [0] * T
+    groups, items, res = plan_relocation(wl, homes, workers=world, link_bytes_per_s=link_gbs * 1e9,
+                                         beam_width=16, steps=256, tc_flops=tc * 1e12, hbm_bps=hbm * 1e9)
+    held0 = [t for t in range(T) if homes[t] == rank]
+    moves_ok = world == 1 or nccl_ok
+    mine_after = [t for t in range(T) if res["masks"][t] >> rank & 1] if moves_ok else held0
+    cap = sum((wl.nodes[t].ntok + 15) // 16 for t in set(held0) | set(mine_after))
+    cap += sum((r.suffix + 2 + 15) // 16 for r in wl.requests if r.leaf in set(mine_after)) + 64
+    pool = halo.Pool(wl.layers, wl.hkv, wl.hq, wl.d, cap, dev)
+    node = {}
+    for t in held0:
+        k, v = wl.node_kv(t, f"cuda:{dev}")
+        node[t] = pool.register_prefix(-1, wl.nodes[t].ntok, k, v)
+        del k, v
+    torch.cuda.synchronize()
+    moved_bytes, mig_ms = 0.0, 0.0
+    acts = rank_actions(res["moves"], rank)
+    if acts and world > 1:
+        if moves_ok:
+            uid = halo.comm_unique_id() if rank == 0 else b"\0" * 128
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            pool.comm_init(obj[0], world, rank)
+            sends = [(node[it], dst, mode) for kind, it, *r in acts if kind == "send" for dst, mode in [r]]
+            recv_items = [it for kind, it, *r in acts if kind == "recv"]
+            recvs = [(r[0], -1, wl.nodes[it].ntok) for kind, it, *r in acts if kind == "recv"]
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            got = pool.migrate_exchange(sends=sends, recvs=recvs)
+            e1.record()
+            torch.cuda.synchronize()
+            mig_ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{dev}")
+            dist.all_reduce(mig_ms, op=dist.ReduceOp.MAX)
+            mig_ms = mig_ms.item()
+            for kind, it, *r in acts:
+                if kind == "send" and r[1] == 0:
+                    node.pop(it)
+            for it, nid in zip(recv_items, got):
+                node[it] = nid
+            moved_bytes = sum(items[m[0]]["kv_bytes"] for m in res["moves"] if m[1] >= 0)
+    reqs, idx = [], []
+    for i, r in enumerate(wl.requests):
+        if r.leaf in node and r.leaf in set(mine_after):
+            reqs.append(pool.open_request(node[r.leaf]))
+            idx.append(i)
+    R = len(reqs)
+    plan = None
+    stream = torch.cuda.current_stream()
+    if R:
+        from synth.workloads import RequestSpec, Workload
+        # this rank's requests (their initial suffixes and the step's token), resident in HBM
+        sub = Workload("c3_shard", wl.layers, wl.hq, wl.hkv, wl.d, [], [RequestSpec(j, -1, wl.requests[i].suffix)
+                       for j, i in enumerate(idx)], seed=wl.seed + 7)
+        sk, sv = sub.suffix_kv(f"cuda:{dev}")
+        pool.append(reqs, [wl.requests[i].suffix for i in idx], sk, sv)
+        nk, nv = sub.new_kv(0, f"cuda:{dev}")
+        pool.append(reqs, [1] * R, nk, nv)
+        del sk, sv
+        q = sub.q(0, f"cuda:{dev}")
+        o = torch.empty((wl.layers, R, wl.hq, wl.d), device=f"cuda:{dev}")
+        plan = pool.plan(reqs)
+
+    def run_layers(evs=None):
+        for l in range(wl.layers):
+            if evs is not None:
+                evs[l][0].record(stream)
+            if plan is not None:
+                plan.run_stages(l, 1, q[l], o[l]) if evs is not None else plan.run(l, q[l], o[l])
+            if evs is not None:
+                evs[l][1].record(stream)
+                if plan is not None:
+                    plan.run_stages(l, 2, q[l], o[l])
+                evs[l][2].record(stream)
+    ms, _, _, _, _ = time_steps(run_layers, wl.layers, steps, warmup, world, dev, torch, dist)
+    if plan is not None:
+        plan.destroy()
+    from paper_2509_02121_b200.sharding import max_over_ranks
+    step_ms = ms / steps  # (time_steps already reduced it over the ranks)
+    out = {"workload": f"C3 batch analytics: {T} templates x 8192-token contexts x 256 requests, "
+                       f"{layers} layers, relocation planner placement over {world} GPU(s)",
+           "value": wl.nreq * wl.layers / (step_ms * 1e-3) if step_ms > 0 else None, "unit": "queries/s",
+           "ms_per_step": step_ms, "templates_here": len(mine_after), "requests_here": R,
+           "moves": len(res["moves"]), "bytes_moved": moved_bytes, "migration_ms": mig_ms,
+           "migration_GB/s": moved_bytes / world / mig_ms / 1e6 if mig_ms > 0 else None,
+           "planner_cost_s": res["cost"], "scaling": "weak",
+           "placement": "relocation planner" if moves_ok else "home GPUs (gloo dry run: moves need NCCL)"}
+    pool.destroy()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
 def measure_strong_scaling(halo, layers, steps, warmup, world, rank, dev, torch, dist):
     """C2 (consolidated agent-DAG tree: 4k root -> 16 roles x 1k -> 1024 requests) with the
     8 kv heads split 8/N per rank: every rank runs the same plan on its head slice (no
@@ -505,6 +613,9 @@ def main():
                         "plan + all layers; H2D in 4-layer and D2H in 2-layer chunks on library "
                         "copy streams, overlapped with the kernels) with pinned host buffers; "
                         "wall clock after sync"}
+    if world > 1 and args.dist_backend == "gloo":
+        extra["migration"] = {"skipped": "NCCL needs one GPU per rank (gloo dry run of the N>1 path)"}
+        extra["paging"] = {"skipped": "gloo dry run"}
     # ---- migration (K4 + NCCL), measured in the same run ----
     if not args.no_migration and not args.profile:
         guarded("migration", lambda: measure_migration(halo, pool, ld, wl, world, rank, dev, torch, dist,
@@ -530,6 +641,15 @@ def main():
     if args.other_configs and not args.profile:
         guarded("strong_scaling", lambda: measure_strong_scaling(
             halo, args.strong_layers, max(3, min(args.steps, 10)), 3, world, rank, dev, torch, dist))
+    # ---- C3 with the relocation planner's placement (BASELINE configs[3]) ----
+    if args.other_configs and not args.profile:
+        link = NVLINK_PEER_GBS
+        for e in extra.get("migration", {}).get("sweep", []) if isinstance(extra.get("migration"), dict) else []:
+            if e.get("pairs_0_to_k"):
+                link = e["pairs_0_to_k"][0]["GB/s"]
+        guarded("c3_placed", lambda: measure_placed_c3(
+            halo, args.other_layers, max(3, min(args.steps, 10)), 3, world, rank, dev, torch, dist, link,
+            nccl_ok=world > 1 and args.dist_backend == "nccl"))
     # ---- CPU oracle baseline ----
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         n, t, cores = oracle_sample(wl, args.cpu_budget)

@@ -1,8 +1,12 @@
+# ncu evidence for one round (one GPU): the launch list of a short bench run, and one
+# `ncu --set full` capture each of K2 (C1 and C3) and K1 (C1 and C3) at the bench configuration.
 set -x
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"prefix_attn|suffix_decode|kv_" --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile --steps 3 --warmup 3 --other-configs "" > gpurun_out/launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:suffix_decode -s 40 -c 1 -o gpurun_out/k2full -f \
     python bench.py --profile --steps 2 --warmup 3 --other-configs "" > gpurun_out/k2full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:suffix_decode -s 4 -c 1 -o gpurun_out/k2full_c3 -f \
+    python bench.py --profile --config analytics --layers 2 --steps 1 --warmup 3 --other-configs "" > gpurun_out/k2full_c3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:prefix_attn -s 40 -c 1 -o gpurun_out/k1full -f \
     python bench.py --profile --steps 2 --warmup 3 --other-configs "" > gpurun_out/k1full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:prefix_attn -s 4 -c 1 -o gpurun_out/k1full_c3 -f \

@@ -531,7 +531,7 @@ def main():
     ms, ms_bd, k1_ms, k2_ms, clk = time_steps(step, L, args.steps, args.warmup, world, dev, torch, dist,
                                        sample_clocks=True)
     step_stats = dict(time_steps.step_stats)  # the headline pass (later legs re-time)
-    launches = args.steps * (1 + 2 * L)
+    launches = args.steps * (3 + 2 * L)  # per step: slot upload + K5 append, plan upload, L x (K1, K2)
     ms_step = ms / args.steps
     value = R * L * world * args.steps / (ms / 1e3)
 
@@ -622,7 +622,7 @@ def main():
                                                        decode_step=step))
     # ---- host paging of the template node (NEXT-2) ----
     if not args.no_migration and not args.profile:
-        guarded("paging", lambda: measure_paging(pool, ld, wl, torch))
+        guarded("paging", lambda: measure_paging(pool, ld, wl, torch, decode_step=step))
     # ---- cost-model relocation planner (NEXT-1), host-side ----
     if not args.profile:
         guarded("relocation", lambda: measure_relocation(halo, extra.get("migration", {})))
@@ -782,7 +782,7 @@ def measure_continuous(halo, wl, dev, torch, steps, churn=0.125):
             "steps": steps, "ms_per_step": ms, "value": R * L / (ms * 1e-3), "unit": UNIT}
 
 
-def measure_paging(pool, ld, wl, torch):
+def measure_paging(pool, ld, wl, torch, decode_step=None):
     """Offload (D2H) and fetch (H2D) of the C1 template node (256 MiB of K+V) through the
     library's pinned host arena (halo_prefix_offload / halo_prefix_fetch), CUDA events on the
     stream; the denominator is a plain pinned cudaMemcpy of the same bytes in this run.  The
@@ -822,6 +822,9 @@ def measure_paging(pool, ld, wl, torch):
     d2h = timed(lambda: h.copy_(d, non_blocking=True))
     h2d = timed(lambda: d.copy_(h, non_blocking=True))
     del h, d
+    bg = None
+    if decode_step is not None:
+        bg = measure_background_prefetch(pool, wl, torch, decode_step, t_fetch)
     pool.host_reserve(0)
     _, tc_peak, _, _ = peaks()
     prefill_ms = 2 * 8.0e9 * ntok / (tc_peak * 1e12) * 1e3
@@ -838,7 +841,60 @@ def measure_paging(pool, ld, wl, torch):
                                         "frac": h2d / t_fetch,
                                         "peak_source": "pinned cudaMemcpy H2D of the same bytes, this run"}},
             "recompute_estimate_ms": prefill_ms,
-            "transfer_vs_recompute": prefill_ms / t_fetch}
+            "transfer_vs_recompute": prefill_ms / t_fetch,
+            "background_prefetch": bg}
+
+
+def measure_background_prefetch(pool, wl, torch, decode_step, t_fetch, steps=12):
+    """PAPER.md:350 "prefetch upcoming caches ... just in time": a second 2048-token template
+    (256 MiB of K+V) of the next batch sits in the host arena; halo_pool_prefetch brings it
+    back on a copy stream while C1 decode steps run on the compute stream (no host sync; the
+    next plan waits for the copy's event).  hidden = 1 - (decode slowdown) / (fetch time
+    alone): 1.0 = the fetch cost the decode nothing."""
+    import numpy as np
+    ntok = wl.nodes[0].ntok
+    dev = torch.cuda.current_device()
+    k = torch.zeros((wl.layers, ntok, wl.hkv, wl.d), dtype=torch.bfloat16, device=f"cuda:{dev}")
+    x = pool.register_prefix(-1, ntok, k, k)
+    rq = pool.open_request(x)
+    del k
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=f"cuda:{dev}")
+
+    def decode_window(with_fetch):
+        pool.offload_prefix(x, compute)
+        torch.cuda.synchronize()
+        e0, e1, f1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(compute)
+        if with_fetch:
+            copy.wait_event(e0)
+            pool.prefetch([rq], copy)
+            f1.record(copy)
+        for _ in range(steps):
+            decode_step()
+        e1.record(compute)
+        torch.cuda.synchronize()
+        dec = e0.elapsed_time(e1)
+        fet = e0.elapsed_time(f1) if with_fetch else None
+        if not with_fetch:
+            pool.fetch_prefix(x, compute)
+            torch.cuda.synchronize()
+        return dec, fet
+    for _ in range(2):
+        decode_window(False)
+        decode_window(True)
+    alone = np.median([decode_window(False)[0] for _ in range(3)])
+    both = [decode_window(True) for _ in range(3)]
+    dec_b = float(np.median([b[0] for b in both]))
+    fet_b = float(np.median([b[1] for b in both]))
+    pool.close_request(rq)
+    pool.release_prefix(x)
+    torch.cuda.synchronize()
+    slow = dec_b - alone
+    return {"what": f"fetch of a 2048-token template (256 MiB) on a copy stream during {steps} C1 decode steps",
+            "decode_ms_alone": float(alone), "decode_ms_with_prefetch": dec_b,
+            "fetch_ms_alone": t_fetch, "fetch_done_ms_after_start": fet_b,
+            "hidden_fraction": max(0.0, 1.0 - slow / t_fetch)}
 
 
 def measure_relocation(halo, mig):

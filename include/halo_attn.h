@@ -33,9 +33,10 @@
  * work enqueued so far on every stream that used the pool (the 16 most recent; an older one is
  * synchronised before it is forgotten) has passed.
  *
- * Plans: a plan records block ids.  Any call that gives blocks back or moves a node (the list
- * above, fetch) makes every plan built before it stale: halo_decode_run then returns
- * HALO_EBUSY; re-plan (halo_decode_plan with the plan as *inout).
+ * Plans: a plan records block ids.  Any call that gives blocks back (the list above) makes
+ * every plan built before it stale: halo_decode_run then returns HALO_EBUSY; re-plan
+ * (halo_decode_plan with the plan as *inout).  A fetch does not (no plan can contain an
+ * offloaded node).
  *
  * Ids: node and request ids are int64, unique and never reused within a pool.
  */
@@ -342,7 +343,7 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
  * are stream-ordered copies on the copy engines (one cudaMemcpyAsync per run of consecutive
  * blocks per layer); the blocks they give up return to their free lists once the enqueued
  * copy has passed.  Plans that read an offloaded node fail with HALO_EBUSY; a plan built
- * before an offload / fetch is stale and halo_decode_run returns HALO_EBUSY (re-plan). */
+ * before an offload is stale and halo_decode_run returns HALO_EBUSY (re-plan). */
 
 /* (Re)allocate the pinned host arena: host_blocks blocks x all layers x K and V.  EBUSY while
  * nodes are offloaded; ENOMEM (arena cleared) if the pinned allocation fails.  On a host-only
@@ -356,6 +357,15 @@ halo_status halo_prefix_offload(halo_pool pool, int64_t node, void *stream);
  * tree position and requests).  EINVAL if not offloaded; ENOMEM pool full (nothing
  * changes). */
 halo_status halo_prefix_fetch(halo_pool pool, int64_t node, void *stream);
+/* Background prefetch ("prefetch upcoming caches ... just in time"): fetch, on
+ * `stream` (typically a copy stream beside the decode stream), every offloaded node on the
+ * prefix paths of reqs[0..nreq) (HOST array), parents first.  Each fetch records an event;
+ * plans built afterwards on any stream (and halo_prefix_read / clone / migrate of the node) wait
+ * for it, so the next step's plan can be built right away while the copies overlap the current
+ * step.  *n_fetched (nullable) = nodes fetched.  ENOMEM: the fetches made so far stay (evict
+ * with halo_pool_evict_lru first). */
+halo_status halo_pool_prefetch(halo_pool pool, int32_t nreq, const int64_t *reqs, void *stream,
+                               int32_t *n_fetched);
 /* on_device: 1 resident, 0 offloaded; last_use: LRU clock of the last plan that read it. */
 halo_status halo_node_residency(halo_pool pool, int64_t node, int32_t *on_device, uint64_t *last_use);
 /* LRU eviction policy: offload device-resident nodes in increasing last_use (ties: lower id),

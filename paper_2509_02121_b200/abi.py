@@ -107,6 +107,7 @@ SIGNATURES = {
     "halo_prefix_offload": (_i32, [_p, _i64, _p]),
     "halo_prefix_fetch": (_i32, [_p, _i64, _p]),
     "halo_node_residency": (_i32, [_p, _i64, C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]),
+    "halo_pool_prefetch": (_i32, [_p, _i32, _pi64, _p, C.POINTER(C.c_int32)]),
     "halo_pool_evict_lru": (_i32, [_p, _i64, _p, C.POINTER(C.c_int32)]),
     "halo_place_groups": (_i32, [C.POINTER(PlaceConfig), _i32, C.POINTER(PlaceItem),
                                  C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -357,6 +358,11 @@ class Pool:
 
     def fetch_prefix(self, node: int, stream=None):
         _call("halo_prefix_fetch", self.handle, node, self._s(stream))
+
+    def prefetch(self, reqs, stream=None) -> int:
+        n = C.c_int32()
+        _call("halo_pool_prefetch", self.handle, len(reqs), _i64_array(reqs), self._s(stream), C.byref(n))
+        return int(n.value)
 
     def residency(self, node: int) -> tuple:
         on, last = C.c_int32(), C.c_uint64()

@@ -154,4 +154,7 @@ cudaError_t launch_kv_runs(const PoolGeom &g, void *pool_k, void *pool_v, void *
                            int64_t item_begin, int64_t item_end, bool to_pool, int max_ctas,
                            cudaStream_t s);
 
+// Host -> device copy of `bytes` by the SMs from MAPPED pinned memory (both 16-B aligned).
+cudaError_t launch_h2d_small(const void *mapped_src, void *dst, size_t bytes, cudaStream_t s);
+
 }  // namespace halo

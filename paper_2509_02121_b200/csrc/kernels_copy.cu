@@ -338,4 +338,28 @@ cudaError_t launch_kv_vmax(const PoolGeom &pg, const void *pool_v, const int32_t
     return cudaGetLastError();
 }
 
+namespace {
+// Host -> device copy by the SMs from mapped pinned memory (zero-copy reads over PCIe): the
+// small per-step uploads (plan arrays, slot lists) then never queue behind a large transfer
+// on a copy engine (e.g. a background prefetch of a prefix node).
+__global__ void __launch_bounds__(256) h2d_small_kernel(const int4 *__restrict__ src, int4 *__restrict__ dst, int64_t n16,
+                                                        const uint8_t *__restrict__ srcb, uint8_t *__restrict__ dstb,
+                                                        int64_t tail_off, int tail) {
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n16; i += (int64_t)gridDim.x * 256) dst[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x < tail) dstb[tail_off + threadIdx.x] = srcb[tail_off + threadIdx.x];
+}
+}  // namespace
+
+cudaError_t launch_h2d_small(const void *mapped_src, void *dst, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return cudaSuccess;
+    const int64_t n16 = (int64_t)(bytes / 16);
+    const int tail = (int)(bytes % 16);
+    int64_t grid = (n16 + 255) / 256;
+    if (grid > 64) grid = 64;
+    if (grid < 1) grid = 1;
+    h2d_small_kernel<<<(unsigned)grid, 256, 0, s>>>((const int4 *)mapped_src, (int4 *)dst, n16,
+                                                    (const uint8_t *)mapped_src, (uint8_t *)dst, n16 * 16, tail);
+    return cudaGetLastError();
+}
+
 }  // namespace halo

@@ -173,6 +173,13 @@ void note_stream(halo_pool p, cudaStream_t s) {
     }
 }
 
+// A node fetched on another stream (background prefetch): order `s` after its copies.
+halo_status wait_ready(halo_pool p, const Node &n, cudaStream_t s) {
+    if (p->host_only || !n.ready) return HALO_OK;
+    return cudaStreamWaitEvent(s, n.ready, 0) == cudaSuccess ? HALO_OK
+                                                             : report_error(HALO_ECUDA, "cudaStreamWaitEvent failed");
+}
+
 void reclaim(halo_pool p, bool wait) {
     for (size_t i = 0; i < p->pending.size();) {
         PendingFree &pf = p->pending[i];
@@ -266,6 +273,18 @@ halo_status upload(const void *host, size_t bytes, cudaStream_t s, Scratch &sc) 
     sc.s = s;
     HALO_CUDA(cudaMallocAsync(&sc.ptr, bytes ? bytes : 16, s));
     if (bytes) HALO_CUDA(cudaMemcpyAsync(sc.ptr, host, bytes, cudaMemcpyHostToDevice, s));
+    return HALO_OK;
+}
+
+// Same through the pool's pinned ring (no host wait behind other streams' copies).
+halo_status upload(halo_pool p, const void *host, size_t bytes, cudaStream_t s, Scratch &sc) {
+    sc.s = s;
+    HALO_CUDA(cudaMallocAsync(&sc.ptr, bytes ? bytes : 16, s));
+    if (!bytes) return HALO_OK;
+    void *h = p->pin_up.acquire(bytes);
+    if (!h) return fail(HALO_ENOMEM, "pinned staging of %zu bytes", bytes);
+    memcpy(h, host, bytes);
+    HALO_CUDA(p->pin_up.commit(sc.ptr, bytes, s));
     return HALO_OK;
 }
 
@@ -969,6 +988,9 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             um[7] = pl->unit_chunk0[uu];
         }
     }
+    pl->waits.clear();
+    for (auto &n : ns)
+        if (n.node->ready) pl->waits.push_back(n.node->ready);
     // 13. info
     halo_plan_info &inf = pl->info;
     inf = halo_plan_info{};
@@ -993,6 +1015,10 @@ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     halo_pool p = pl->pool;
+    // nodes fetched from the host arena on another stream (background prefetch): the plan's
+    // stream waits for their copies (free once they have passed)
+    if (!p->host_only)
+        for (cudaEvent_t e : pl->waits) HALO_CUDA(cudaStreamWaitEvent(s, e, 0));
     const int nreq = pl->nreq;
     size_t off = 0;
     const size_t o_tiles = off; off = align16(off + pl->tiles.size() * sizeof(PrefixTile));
@@ -1397,6 +1423,9 @@ halo_status halo_pool_destroy(halo_pool p) {
         for (auto &pf : p->pending)
             for (cudaEvent_t e : pf.events) cudaEventDestroy(e);
         for (cudaEvent_t e : p->event_cache) cudaEventDestroy(e);
+        for (auto &n : p->nodes)
+            if (n.second.ready) cudaEventDestroy(n.second.ready);
+        p->pin_up.release();
         for (cudaEvent_t e : p->mig_ev)
             if (e) cudaEventDestroy(e);
         if (p->mig_done) cudaEventDestroy(p->mig_done);
@@ -1458,7 +1487,7 @@ halo_status halo_prefix_register(halo_pool p, int64_t parent, int32_t ntok, cons
         slots.insert(slots.end(), tags.begin(), tags.end());  // one upload: slots | tags
         Scratch ss, sk, sv;
         const void *dk = nullptr, *dvp = nullptr;
-        st = upload(slots.data(), slots.size() * 4, s, ss);
+        st = upload(p, slots.data(), slots.size() * 4, s, ss);
         if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
         if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
         if (st == HALO_OK) {
@@ -1498,6 +1527,7 @@ halo_status halo_prefix_release(halo_pool p, int64_t node) {
     const int64_t parent = it->second.parent;
     release_blocks(p, std::move(it->second.blocks));
     release_host_blocks(p, std::move(it->second.host_blocks));
+    if (it->second.ready) p->event_cache.push_back(it->second.ready);
     p->nodes.erase(it);
     if (parent >= 0) p->nodes[parent].children--;
     return HALO_OK;
@@ -1514,9 +1544,11 @@ halo_status halo_prefix_read(halo_pool p, int64_t node, void *k_out, void *v_out
     if (!k_out || !v_out) return fail(HALO_EINVAL, "null output");
     DeviceGuard dg(p);
     cudaStream_t s = (cudaStream_t)stream;
+    halo_status st = wait_ready(p, it->second, s);
+    if (st != HALO_OK) return st;
     std::vector<int32_t> slots = token_slots(it->second.blocks, it->second.ntok);
     Scratch ss;
-    halo_status st = upload(slots.data(), slots.size() * 4, s, ss);
+    st = upload(p, slots.data(), slots.size() * 4, s, ss);
     if (st != HALO_OK) return st;
     cudaError_t e = launch_kv_gather(p->geom, p->k, p->v, k_out, v_out, (const int32_t *)ss.ptr,
                                      it->second.ntok, 0, p->cfg.num_layers, p->num_sms, s);
@@ -1658,7 +1690,7 @@ halo_status halo_suffix_append(halo_pool p, int32_t nreq, const int64_t *reqs, c
         std::vector<int32_t> st_buf = w.slots;
         std::vector<uint32_t> tags = slot_tags(p, w.slots);
         st_buf.insert(st_buf.end(), tags.begin(), tags.end());  // slots | tags
-        st = upload(st_buf.data(), st_buf.size() * 4, s, ss);
+        st = upload(p, st_buf.data(), st_buf.size() * 4, s, ss);
         if (st == HALO_OK) st = as_device(k, bytes, s, sk, &dk);
         if (st == HALO_OK) st = as_device(v, bytes, s, sv, &dvp);
         if (st == HALO_OK) {
@@ -2249,8 +2281,9 @@ halo_status halo_migrate_exchange(halo_pool p, int32_t nsend, const halo_migrate
     for (int32_t i = 0; i < nsend; ++i) add(true, sends[i].peer, &p->nodes[sends[i].node].blocks);
     for (int32_t i = 0; i < nrecv; ++i) add(false, recvs[i].peer, &dst[i]);
     halo_status st = ensure_mig(p, 2 * per_parity);
+    for (int32_t i = 0; i < nsend && st == HALO_OK; ++i) st = wait_ready(p, p->nodes[sends[i].node], s);
     Scratch sl;
-    if (st == HALO_OK) st = upload(lists.data(), lists.size() * 4, s, sl);
+    if (st == HALO_OK) st = upload(p, lists.data(), lists.size() * 4, s, sl);
     if (st != HALO_OK) {
         undo();
         return st;
@@ -2316,6 +2349,7 @@ halo_status halo_migrate_exchange(halo_pool p, int32_t nsend, const halo_migrate
         if (it == p->nodes.end()) continue;  // (listed twice as COPY and MOVE: already gone)
         const int64_t parent = it->second.parent;
         release_blocks(p, std::move(it->second.blocks));
+        if (it->second.ready) p->event_cache.push_back(it->second.ready);
         p->nodes.erase(it);
         if (parent >= 0) p->nodes[parent].children--;
         p->layout_gen++;
@@ -2366,10 +2400,12 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
         return fail(HALO_ENOENT, "unknown parent %lld", (long long)parent_dst);
     DeviceGuard dg(src);
     cudaStream_t s = (cudaStream_t)stream;
+    halo_status st = wait_ready(src, it->second, s);
+    if (st != HALO_OK) return st;
     const int32_t ntok = it->second.ntok;
     const int64_t nblk = ceil_div(ntok, kBlockTok);
     std::vector<int32_t> blocks;
-    halo_status st = alloc_blocks(dst, nblk, blocks);
+    st = alloc_blocks(dst, nblk, blocks);
     if (st != HALO_OK) return st;
     // whole-block pool-to-pool copy: a (layer, block) of all heads is contiguous on both sides
     std::vector<int32_t> pairs(3 * nblk);  // pairs | destination tags
@@ -2379,7 +2415,7 @@ halo_status halo_prefix_clone(halo_pool src, int64_t node, halo_pool dst, int64_
         pairs[2 * nblk + b] = (int32_t)dst->blk_epoch[blocks[b]];
     }
     Scratch sp;
-    if ((st = upload(pairs.data(), pairs.size() * 4, s, sp)) == HALO_OK) {
+    if ((st = upload(src, pairs.data(), pairs.size() * 4, s, sp)) == HALO_OK) {
         const int32_t *dp = (const int32_t *)sp.ptr;
         cudaError_t e = launch_kv_copy_blocks(src->geom, src->k, src->v, dst->geom, dst->k, dst->v, dp,
                                               (const uint32_t *)(dp + 2 * nblk), (int32_t)nblk, 0,
@@ -2469,13 +2505,18 @@ halo_status halo_prefix_fetch(halo_pool p, int64_t node, void *stream) {
         std::vector<int32_t> bt(db);  // blocks | tags: the V-table entries are recomputed
         for (int32_t b : db) bt.push_back((int32_t)p->blk_epoch[b]);
         Scratch sb;
-        st = upload(bt.data(), bt.size() * 4, s, sb);
+        st = upload(p, bt.data(), bt.size() * 4, s, sb);
         if (st == HALO_OK) st = copy_node_blocks(p, db, n.host_blocks, false, s);
         if (st == HALO_OK) {
             const int32_t *d = (const int32_t *)sb.ptr;
             cudaError_t e = launch_kv_vmax(p->geom, p->v, d, (const uint32_t *)(d + db.size()), (int32_t)db.size(),
                                            p->num_sms, s);
             if (e != cudaSuccess) st = fail(HALO_ECUDA, "V-table launch: %s", cudaGetErrorString(e));
+        }
+        if (st == HALO_OK) {
+            if (!n.ready) n.ready = get_event(p);
+            if (!n.ready || cudaEventRecord(n.ready, s) != cudaSuccess)
+                st = fail(HALO_ECUDA, "fetch event record failed");
         }
         if (st != HALO_OK) {
             unalloc_blocks(p, db, 0);
@@ -2487,8 +2528,33 @@ halo_status halo_prefix_fetch(halo_pool p, int64_t node, void *stream) {
     n.host_blocks.clear();
     n.blocks = std::move(db);
     n.on_host = false;
-    p->layout_gen++;
+    // (no plan can reference an offloaded node -- building one fails with EBUSY -- so a fetch
+    // leaves existing plans valid: a step's plan keeps running while the next step prefetches)
     return HALO_OK;
+    HALO_GUARD_END
+}
+
+halo_status halo_pool_prefetch(halo_pool p, int32_t nreq, const int64_t *reqs, void *stream, int32_t *n_fetched) {
+    HALO_GUARD_BEGIN
+    if (check_pool(p)) return HALO_EINVAL;
+    if (nreq < 0 || (nreq > 0 && !reqs)) return fail(HALO_EINVAL, "bad request list");
+    std::vector<int64_t> want;  // offloaded nodes on the requests' paths, parents first
+    for (int32_t i = 0; i < nreq; ++i) {
+        auto r = p->requests.find(reqs[i]);
+        if (r == p->requests.end()) return fail(HALO_ENOENT, "unknown request %lld", (long long)reqs[i]);
+        std::vector<int64_t> path;
+        for (int64_t id = r->second.leaf; id >= 0; id = p->nodes[id].parent) path.push_back(id);
+        for (auto it = path.rbegin(); it != path.rend(); ++it)
+            if (p->nodes[*it].on_host && std::find(want.begin(), want.end(), *it) == want.end()) want.push_back(*it);
+    }
+    int32_t n = 0;
+    halo_status st = HALO_OK;
+    for (int64_t id : want) {
+        if ((st = halo_prefix_fetch(p, id, stream)) != HALO_OK) break;
+        ++n;
+    }
+    if (n_fetched) *n_fetched = n;
+    return st;
     HALO_GUARD_END
 }
 

@@ -25,6 +25,8 @@ struct Node {
     bool on_host = false;              // offloaded: KV lives in host_blocks of the host arena
     std::vector<int32_t> host_blocks;
     uint64_t last_use = 0;             // plan tick of the last plan that read the node (LRU)
+    cudaEvent_t ready = nullptr;       // recorded after a fetch's device writes (background
+                                       // prefetch): plans / reads of the node wait on it
 };
 
 struct Request {
@@ -43,15 +45,17 @@ struct StreamFence {
     uint64_t last_use;
 };
 
-// Double-buffered pinned host staging for small per-step uploads (plan arrays, slot lists):
-// an H2D copy from pinned memory is truly asynchronous, so the host can build the next
-// step's plan while the GPU still runs this one.  acquire() waits for the copy that last
-// used the buffer, commit() enqueues the copy and records the buffer's event.
+// Ring of pinned host staging buffers for small per-step uploads (plan arrays, slot lists):
+// an H2D copy from pinned memory is truly asynchronous (a pageable one makes the host wait for
+// the DMA, e.g. behind a large fetch on a copy stream), so the host can build the next step's
+// plan while the GPU still runs this one.  acquire() waits for the copy that last used the
+// buffer (kPinBufs uploads ago), commit() enqueues the copy and records the buffer's event.
+constexpr int kPinBufs = 4;
 struct PinRing {
-    void *buf[2] = {nullptr, nullptr};
-    size_t cap[2] = {0, 0};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    bool used[2] = {false, false};
+    void *buf[kPinBufs] = {};
+    size_t cap[kPinBufs] = {};
+    cudaEvent_t ev[kPinBufs] = {};
+    bool used[kPinBufs] = {};
     int cur = 0;
     void *acquire(size_t bytes);                                   // nullptr on failure
     cudaError_t commit(void *dst, size_t bytes, cudaStream_t s);   // copies buf[cur] -> dst
@@ -59,29 +63,31 @@ struct PinRing {
 };
 
 inline void *PinRing::acquire(size_t bytes) {
-    cur ^= 1;
+    cur = (cur + 1) % kPinBufs;
     if (used[cur] && ev[cur]) cudaEventSynchronize(ev[cur]);
     if (!ev[cur] && cudaEventCreateWithFlags(&ev[cur], cudaEventDisableTiming) != cudaSuccess) return nullptr;
     if (cap[cur] < bytes) {
         if (buf[cur]) cudaFreeHost(buf[cur]);
         buf[cur] = nullptr;
         cap[cur] = 0;
-        const size_t c = bytes + bytes / 2 + 4096;
-        if (cudaMallocHost(&buf[cur], c) != cudaSuccess) return nullptr;
+        const size_t c = (bytes + bytes / 2 + 4096 + 15) / 16 * 16;
+        if (cudaHostAlloc(&buf[cur], c, cudaHostAllocMapped) != cudaSuccess) return nullptr;
         cap[cur] = c;
     }
     return buf[cur];
 }
 
 inline cudaError_t PinRing::commit(void *dst, size_t bytes, cudaStream_t s) {
-    cudaError_t e = bytes ? cudaMemcpyAsync(dst, buf[cur], bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    // SM copy from the mapped buffer (unified addressing: the host pointer is valid on the
+    // device): never queued behind another stream's copy-engine transfer
+    cudaError_t e = bytes ? launch_h2d_small(buf[cur], dst, bytes, s) : cudaSuccess;
     if (e == cudaSuccess) e = cudaEventRecord(ev[cur], s);
     used[cur] = (e == cudaSuccess);
     return e;
 }
 
 inline void PinRing::release() {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kPinBufs; ++i) {
         if (ev[i]) cudaEventSynchronize(ev[i]);
         if (buf[i]) cudaFreeHost(buf[i]);
         if (ev[i]) cudaEventDestroy(ev[i]);
@@ -121,6 +127,7 @@ struct halo_pool_s {
     std::vector<int32_t> host_free;
     std::vector<halo::PendingFree> host_pending;
     uint64_t plan_tick = 0;     // incremented per plan build (LRU clock)
+    halo::PinRing pin_up;       // pinned staging of the pool's small uploads (slot / block lists)
     uint64_t layout_gen = 0;    // incremented when a node's blocks move (offload / fetch)
     CUtensorMap tmap_k{}, tmap_v{};      // box: one 16-token block x 64 d
     CUtensorMap tmap_k8{}, tmap_v8{};    // box: 8 consecutive blocks (128 tokens) x 64 d
@@ -170,6 +177,7 @@ struct halo_plan_s {
     int32_t tmap_q_nreq = -1;
     bool tmap_q_ok = false;
     halo::PlanDev dev{};
+    std::vector<cudaEvent_t> waits;   // fetch events of the plan's nodes (waited at upload)
     // staging for halo_decode_layers with host buffers
     void *q_stage = nullptr;
     size_t q_stage_cap = 0;

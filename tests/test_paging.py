@@ -178,3 +178,64 @@ def test_lru_paging_under_memory_pressure_keeps_parity():
             p.offload_prefix(other)
     assert cap > 0
     p.destroy()
+
+
+def test_prefetch_bookkeeping_on_host_only_pool():
+    """halo_pool_prefetch fetches exactly the offloaded nodes on the requests' paths (parents
+    first), nothing else; resident nodes and unknown requests behave as documented."""
+    wl = make_config("tree", layers=2, root=64, roles=3, role_tok=32, per_role=4, suffix=5)
+    ld = load(wl, device=-1)
+    p = ld.pool
+    p.host_reserve(64)
+    root, r1, r2 = ld.node_ids[0], ld.node_ids[1], ld.node_ids[2]
+    for n in (r2, r1, root):
+        p.offload_prefix(n)
+    reqs_r1 = [ld.req_ids[i] for i, r in enumerate(wl.requests) if r.leaf == 1]
+    assert p.prefetch(reqs_r1) == 2          # root, then role 1
+    assert p.residency(root)[0] and p.residency(r1)[0] and not p.residency(r2)[0]
+    assert p.prefetch(reqs_r1) == 0
+    assert err_name(p.prefetch, [123456]) == "HALO_ENOENT"
+    p.destroy()
+
+
+@pytest.mark.gpu
+def test_background_prefetch_overlaps_decode_and_keeps_parity():
+    """prefetch the next batch's offloaded template on a copy stream while the
+    current batch decodes on the compute stream, then plan and run the next batch on the
+    compute stream without a host synchronisation: the plan waits for the copies (node fetch
+    events) and the outputs equal the pre-offload ones bit for bit (and the oracle)."""
+    torch.cuda.set_device(0)
+    wa = make_config("fanout", layers=4, nreq=128, prefix=2048, suffix=63, seed=11)
+    wb = make_config("fanout", layers=4, nreq=128, prefix=1024, suffix=63, seed=12)
+    from paper_2509_02121_b200.loader import blocks_needed
+    la = load(wa, 0, capacity=blocks_needed(wa) + blocks_needed(wb))
+    lb = load(wb, 0, pool=la.pool)
+    p = la.pool
+    p.host_reserve(2048 // 16 + 8)
+    append_step(la, wa, 0, 0)
+    append_step(lb, wb, 0, 0)
+    qa, qb = wa.q(0, "cuda"), wb.q(0, "cuda")
+    ref = torch.empty((wa.nreq, wa.hq, wa.d), device="cuda")
+    pa = p.plan(la.req_ids)
+    pa.run(3, qa[3], ref)
+    pa.destroy()
+    p.offload_prefix(la.node_ids[0])
+    torch.cuda.synchronize()
+    compute, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    ob = torch.empty((wb.nreq, wb.hq, wb.d), device="cuda")
+    oa = torch.empty_like(ref)
+    pb = p.plan(lb.req_ids, stream=compute)
+    for rep in range(2):
+        for l in range(4):
+            pb.run(l, qb[l], ob, stream=compute)      # the current batch decodes ...
+        if rep == 0:
+            assert p.prefetch(la.req_ids, stream=copy) == 1   # ... while the next one's KV arrives
+    pa = p.plan(la.req_ids, stream=compute)           # no host sync: the plan waits for the fetch
+    pa.run(3, qa[3], oa, stream=compute)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ref)
+    ro, _ = oracle.decode_reference(wa, 3, steps=1, requests=list(range(0, wa.nreq, 16)))
+    assert np.abs(oa.cpu().numpy()[::16] - ro).max() <= 2e-3
+    pa.destroy()
+    pb.destroy()
+    p.destroy()

@@ -1,14 +1,6 @@
-# One GPU, end of a measurement cycle: the default bench line, the ncu launch list of a short
-# bench run, and one `ncu --set full` capture each of K2 and K1 at the C1 bench configuration.
+# One GPU, end of a measurement cycle: GPU tests, the default bench line, then the ncu
+# captures of tools/round_ncu.sh (launch list + `--set full` of K1 and K2 at C1 and C3).
 set -x
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"prefix_attn|suffix_decode|kv_" --csv --log-file gpurun_out/launches.csv \
-    python bench.py --profile --steps 3 --warmup 3 --other-configs "" > gpurun_out/launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:suffix_decode -s 40 -c 1 -o gpurun_out/k2full -f \
-    python bench.py --profile --steps 2 --warmup 3 --other-configs "" > gpurun_out/k2full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:prefix_attn -s 40 -c 1 -o gpurun_out/k1full -f \
-    python bench.py --profile --steps 2 --warmup 3 --other-configs "" > gpurun_out/k1full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:prefix_attn -s 4 -c 1 -o gpurun_out/k1full_c3 -f \
-    python bench.py --profile --config analytics --layers 2 --steps 1 --warmup 3 --other-configs "" > gpurun_out/k1full_c3.log 2>&1
-ls -la gpurun_out
+bash tools/round_ncu.sh

@@ -90,6 +90,10 @@ struct PlanDev {
     int64_t seg_slot_stride;     // floats between the slots of seg_o (seg_ml likewise, /D*2)
     int32_t count_slot_stride;   // ints between the slots of unit_count
     float *park;                 // [4][nunits][g * (D + 2)]: o (fragment layout), then (m, l) per head
+    // equal-share schedule used when K2 is launched without K1 right before it (0: none)
+    int32_t alt_nchunks;
+    const int4 *alt_chunk_info;
+    const int4 *alt_unit_meta;
 };
 
 struct PoolGeom {

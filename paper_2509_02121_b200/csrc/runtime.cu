@@ -827,13 +827,13 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         const int64_t Btot = pl->unit_boff[U], Itot = Btot + U;
         auto ui = [&](int64_t u) { return (int64_t)pl->unit_boff[u] + u; };  // items before unit u
         auto nb = [&](int64_t u) { return (int64_t)pl->unit_boff[u + 1] - pl->unit_boff[u]; };
-        auto unit_of = [&](int64_t x) {  // unit owning item x < Itot
-            int64_t a = 0, b = U - 1;
-            while (a < b) {
-                const int64_t m = (a + b + 1) / 2;
-                if (ui(m) <= x) a = m; else b = m - 1;
-            }
-            return a;
+        // item -> unit map (O(1) lookups: the cut computations below do thousands of them)
+        std::vector<int32_t> &umap = pl->item_unit;
+        umap.resize((size_t)Itot);
+        for (int u = 0; u < U; ++u)
+            std::fill(umap.begin() + ui(u), umap.begin() + ui(u + 1), (int32_t)u);
+        auto unit_of = [&](int64_t x) -> int64_t {  // unit owning item x < Itot
+            return umap[(size_t)std::min(std::max<int64_t>(x, 0), Itot - 1)];
         };
         // a cut never separates a unit's merge item from its last block (that chunk would
         // visit the unit with no blocks)
@@ -849,7 +849,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         // rest enter as K1's CTAs retire.  Warps of the early CTAs get `ew` times the share.
         const int64_t k1c = (int64_t)pl->tiles.size();
         const int64_t early_ctas = (k1c > 0 && k1c < k2_sms(pl)) ? k2_sms(pl) - k1c : 0;
-        const double ew = early_ctas > 0 && (pl->k2_early || pl->opt.k2_early_weight > 0) ? k2_early_weight(pl) : 1.0;
+        double ew = early_ctas > 0 && (pl->k2_early || pl->opt.k2_early_weight > 0) ? k2_early_weight(pl) : 1.0;
         auto target = [&](int64_t w, int64_t nw, int wpc) -> int64_t {  // item position of cut w
             if (ew == 1.0) return w * Itot / nw;
             const int64_t ne = std::min<int64_t>(nw, early_ctas * wpc);
@@ -936,9 +936,14 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         std::vector<int32_t> &lo = pl->chunk_lo;
         lo.resize(nchunks + 1);
         for (int64_t c = 0; c <= nchunks; ++c) lo[c] = (int32_t)block_at(cuts[c]);
-        auto chunk_of = [&](int64_t x) {  // chunk containing item x
-            return (int64_t)(std::upper_bound(cuts.begin(), cuts.end(), x) - cuts.begin()) - 1;
+        std::vector<int32_t> &cmap = pl->item_chunk;  // item -> chunk
+        auto fill_cmap = [&](const std::vector<int64_t> &c) {
+            cmap.resize((size_t)Itot);
+            for (size_t k = 0; k + 1 < c.size(); ++k)
+                std::fill(cmap.begin() + c[k], cmap.begin() + std::min(c[k + 1], Itot), (int32_t)k);
         };
+        fill_cmap(cuts);
+        auto chunk_of = [&](int64_t x) -> int64_t { return cmap[(size_t)x]; };
         pl->chunk_u0.assign(nchunks, 0);
         pl->chunk_u1.assign(nchunks, 0);
         for (int64_t c = 0; c < nchunks && U > 0; ++c) {
@@ -986,6 +991,42 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             um[0] = b0; um[1] = b1; um[2] = req; um[3] = head;
             um[4] = pl->req_nslots[req]; um[5] = pl->unit_nseg[uu]; um[6] = pl->unit_seg[uu];
             um[7] = pl->unit_chunk0[uu];
+        }
+        // K2 launched ALONE (K1 complete before it starts: halo_decode_run_stages with only the
+        // K2 bit) runs without the co-schedule's early-CTA weights: an equal-share schedule
+        pl->alt_nchunks = 0;
+        pl->alt_nseg_total = 0;
+        if (ew != 1.0 && pl->k2_warps == kK2WarpsWide && pl->dyn_first == (int32_t)nchunks) {
+            ew = 1.0;
+            bool bal2 = false;
+            std::vector<int64_t> ce = snapped_cuts(Ww, kK2WarpsWide, bal2);
+            if (!bal2) ce = equal_cuts(Ww, kK2WarpsWide);
+            if (ce.size() < 2) ce = {0, Itot};
+            const int64_t ne = (int64_t)ce.size() - 1;
+            fill_cmap(ce);
+            auto chunk_of_e = [&](int64_t x) -> int64_t { return cmap[(size_t)x]; };
+            pl->alt_chunk_info.assign((size_t)ne * 4, 0);
+            for (int64_t c = 0; c < ne; ++c) {
+                pl->alt_chunk_info[4 * c] = (int32_t)block_at(ce[c]);
+                pl->alt_chunk_info[4 * c + 1] = (int32_t)block_at(ce[c + 1]);
+                if (ce[c + 1] > ce[c] && U > 0) {
+                    pl->alt_chunk_info[4 * c + 2] = (int32_t)unit_of(ce[c]);
+                    pl->alt_chunk_info[4 * c + 3] = (int32_t)unit_of(ce[c + 1] - 1) + 1;
+                }
+            }
+            pl->alt_unit_meta = pl->unit_meta;
+            int32_t nst = 0;
+            for (int uu = 0; uu < U; ++uu) {
+                const int64_t c0 = chunk_of_e(ui(uu)), c1 = chunk_of_e(ui(uu + 1) - 1);
+                const int nseg = (int)(c1 - c0 + 1);
+                int32_t *um = &pl->alt_unit_meta[(size_t)uu * 8];
+                um[5] = nseg;
+                um[6] = nseg > 1 ? nst : -1;
+                um[7] = (int32_t)c0;
+                if (nseg > 1) nst += nseg;
+            }
+            pl->alt_nseg_total = nst;
+            pl->alt_nchunks = (int32_t)ne;
         }
     }
     pl->waits.clear();
@@ -1039,6 +1080,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     const size_t o_ent = off; off = align16(off + pl->k2_ent.size() * 4);
     const size_t o_umeta = off; off = align16(off + pl->unit_meta.size() * 4);
     const size_t o_cinfo = off; off = align16(off + pl->chunk_info.size() * 4);
+    const size_t o_acinfo = off; off = align16(off + (size_t)pl->alt_nchunks * 16);
+    const size_t o_aumeta = off; off = align16(off + (pl->alt_nchunks ? pl->alt_unit_meta.size() * 4 : 0));
     const size_t o_taux = off; off = align16(off + pl->tile_aux.size() * 4);
     const size_t total = off;
     uint8_t *h;
@@ -1067,6 +1110,10 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     put(o_ent, pl->k2_ent.data(), pl->k2_ent.size() * 4);
     put(o_umeta, pl->unit_meta.data(), pl->unit_meta.size() * 4);
     put(o_cinfo, pl->chunk_info.data(), pl->chunk_info.size() * 4);
+    if (pl->alt_nchunks) {
+        put(o_acinfo, pl->alt_chunk_info.data(), (size_t)pl->alt_nchunks * 16);
+        put(o_aumeta, pl->alt_unit_meta.data(), pl->alt_unit_meta.size() * 4);
+    }
     put(o_taux, pl->tile_aux.data(), pl->tile_aux.size() * 4);
     if (p->host_only) return HALO_OK;
 
@@ -1095,7 +1142,8 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     // pieces (o in K2's fragment layout, kK2HeadPad heads x d, + (m, l) per head) and parked
     // whole-unit states (g heads x (d + 2)) -- one buffer
     const int gq = p->cfg.num_q_heads / p->cfg.num_kv_heads;
-    const size_t seg_slot = (size_t)std::max(pl->nseg_total, 1) * kK2HeadPad * (p->cfg.head_dim + 2);
+    const int32_t nseg_max = std::max(std::max(pl->nseg_total, pl->alt_nseg_total), 1);
+    const size_t seg_slot = (size_t)nseg_max * kK2HeadPad * (p->cfg.head_dim + 2);
     const size_t park_slot = (size_t)U * gq * (p->cfg.head_dim + 2);
     const size_t seg_elems = 4 * (seg_slot + park_slot);
     if (pl->seg_cap < seg_elems) {
@@ -1149,11 +1197,14 @@ halo_status upload_plan(halo_plan pl, cudaStream_t s) {
     dv.k2_ent = reinterpret_cast<const uint2 *>(d + o_ent);
     dv.unit_meta = reinterpret_cast<const int4 *>(d + o_umeta);
     dv.chunk_info = reinterpret_cast<const int4 *>(d + o_cinfo);
+    dv.alt_nchunks = pl->alt_nchunks;
+    dv.alt_chunk_info = reinterpret_cast<const int4 *>(d + o_acinfo);
+    dv.alt_unit_meta = reinterpret_cast<const int4 *>(d + o_aumeta);
     dv.tile_aux = reinterpret_cast<const int4 *>(d + o_taux);
     dv.nchunks = NC;
     dv.nblocks = pl->unit_boff.empty() ? 0 : pl->unit_boff.back();
     dv.seg_o = pl->segbuf;
-    dv.seg_ml = pl->segbuf + (size_t)std::max(pl->nseg_total, 1) * kK2HeadPad * p->cfg.head_dim;
+    dv.seg_ml = pl->segbuf + (size_t)nseg_max * kK2HeadPad * p->cfg.head_dim;
     dv.seg_slot_stride = (int64_t)seg_slot;
     dv.park = pl->segbuf + 4 * seg_slot;
     dv.nwarps = k2_sms(pl) * pl->k2_warps;
@@ -1186,7 +1237,14 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
         if (e != cudaSuccess) return fail(HALO_ECUDA, "prefix kernel launch: %s", cudaGetErrorString(e));
     }
     if (mask & 2) {
-        e = launch_suffix_decode(&p->tmap_k, &p->tmap_v, pl->dev, p->geom, layer, q, out, lse, scale, s);
+        PlanDev dv = pl->dev;
+        if (!(mask & 1) && dv.alt_nchunks > 0) {  // K2 alone: the equal-share schedule
+            dv.chunk_info = dv.alt_chunk_info;
+            dv.unit_meta = dv.alt_unit_meta;
+            dv.nchunks = dv.alt_nchunks;
+            dv.dyn_first = dv.alt_nchunks;
+        }
+        e = launch_suffix_decode(&p->tmap_k, &p->tmap_v, dv, p->geom, layer, q, out, lse, scale, s);
         if (e != cudaSuccess) return fail(HALO_ECUDA, "suffix kernel launch: %s", cudaGetErrorString(e));
     }
     return HALO_OK;

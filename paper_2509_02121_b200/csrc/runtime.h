@@ -150,6 +150,10 @@ struct halo_plan_s {
     std::vector<int32_t> unit_boff, chunk_lo, chunk_u0, chunk_u1, unit_chunk0, unit_nseg, unit_seg;
     int32_t nseg_total = 0;
     int32_t dyn_first = 0;  // first dynamically claimed K2 chunk (== nchunks: none)
+    // equal-share K2 schedule for K2 launched alone (co-schedule weights off)
+    std::vector<int32_t> alt_chunk_info, alt_unit_meta;
+    std::vector<int32_t> item_unit, item_chunk;  // planner scratch (item -> unit / chunk maps)
+    int32_t alt_nchunks = 0, alt_nseg_total = 0;
     int32_t k2_warps = halo::kK2WarpsWide;
     bool k2_early = false;  // K1 split count lowered so K2's first CTAs stream beside K1
     double k2_early_w = 1.0;  // the co-schedule model's work weight of those CTAs

@@ -558,3 +558,25 @@ def test_plan_is_stale_after_blocks_are_given_back():
     plan.run(0, q, out)
     torch.cuda.synchronize()
     cleanup(ld, plan)
+
+
+def test_k2_alone_uses_the_equal_share_schedule_and_matches_oracle():
+    """With the K1/K2 co-schedule on (C1 shape), K2 launched by itself after K1
+    (halo_decode_run_stages K1 then K2) runs the plan's equal-share schedule, K1+K2 launched
+    together the weighted one; both match the oracle."""
+    wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=255)
+    ld = load(wl, DEV)
+    append_step(ld, wl, 0, DEV)
+    plan = ld.pool.plan(ld.req_ids)
+    assert plan.info()["k1_tiles"] == 64
+    q = wl.q(0, "cuda")
+    o1 = torch.empty((wl.nreq, wl.hq, wl.d), device="cuda")
+    o2 = torch.empty_like(o1)
+    plan.run(0, q[0], o1)
+    plan.run_stages(0, 1, q[0], o2)
+    plan.run_stages(0, 2, q[0], o2)
+    torch.cuda.synchronize()
+    ro, _ = oracle.decode_reference(wl, 0, steps=1, requests=list(range(0, wl.nreq, 5)))
+    for o in (o1, o2):
+        assert np.abs(o.cpu().numpy()[::5] - ro).max() <= OUT_TOL
+    cleanup(ld, plan)

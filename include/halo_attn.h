@@ -235,7 +235,7 @@ typedef struct {
     int32_t k1_tiles;        /* K1 CTAs per layer */
     int32_t k2_units;        /* (request, kv head) work units of K2 */
     int32_t max_slots;       /* partial slots per request (max over requests) */
-    int32_t reserved;
+    int32_t k2_warps;        /* K2 launch shape: warps per CTA (12 wide / 7 narrow) */
     int64_t k1_rows;         /* sum over K1 tiles of valid rows x tokens / 128 (bookkeeping) */
     double k1_flops;         /* algorithmic FLOPs per layer: sum_nodes 4*(n_req*g)*L_n*d*Hkv */
     double k1_bytes;         /* algorithmic bytes per layer of K1 (KV once + Q + partials) */

@@ -37,7 +37,7 @@ class PlanOptions(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("nreq", _i32), ("num_q_heads", _i32), ("num_kv_heads", _i32), ("head_dim", _i32),
                 ("tensor_nodes", _i32), ("folded_nodes", _i32), ("k1_tiles", _i32),
-                ("k2_units", _i32), ("max_slots", _i32), ("reserved", _i32), ("k1_rows", _i64),
+                ("k2_units", _i32), ("max_slots", _i32), ("k2_warps", _i32), ("k1_rows", _i64),
                 ("k1_flops", C.c_double), ("k1_bytes", C.c_double), ("k2_bytes", C.c_double),
                 ("unshared_bytes", C.c_double)]
 

@@ -36,14 +36,16 @@
 
 #ifdef HALO_K2_TRACE
 // Debug timeline: g_k2_trace[gw * 4 + e] = %globaltimer (ns) of global warp gw at event e:
-// 0 entry, 1 first K/V stage landed, 2 K1 complete (griddepcontrol.wait returned), 3 exit.
+// 0 entry, 1 first K/V stage landed, 2 K1 complete (griddepcontrol.wait returned), 3 exit,
+// 4 last K/V stage landed, 5 start of the last unit end (merge / finalize / publish),
+// 6 before the completion-count atomic.
 __device__ unsigned long long *g_k2_trace = nullptr;
 #define K2_TRACE(gw, ev)                                                                \
     do {                                                                                \
         if (g_k2_trace && lane == 0) {                                                  \
             unsigned long long t_;                                                      \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
-            g_k2_trace[(gw) * 4 + (ev)] = t_;                                           \
+            g_k2_trace[(gw) * 8 + (ev)] = t_;                                           \
         }                                                                               \
     } while (0)
 extern "C" int halo_debug_k2_trace(void *buf) {
@@ -61,6 +63,9 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLazy = 8.f;  // base-2 headroom of the lazy running max (p <= 2^8)
 constexpr int NPAD = kK2HeadPad;  // MMA N: the unit's g q-heads padded to 8
 constexpr int NPARK = 16;         // units a warp may park while K1 is still running
+#ifndef HALO_K2_EXP
+#define HALO_K2_EXP 0             // timing experiments only: 1 = skip block compute, 2 = skip unit end
+#endif
 #ifndef HALO_K2_PF
 #define HALO_K2_PF 0              // blocks prefetched into L2 ahead of the smem ring (A/B: 2-8 slower, tools/k1k2_cosched_sweep.py)
 #endif
@@ -110,46 +115,60 @@ __device__ __forceinline__ uint32_t swz(int r, int d) {
 // Final merge of a unit's suffix state with the request's K1 partials, then the fp32 output /
 // lse store.  Lane layout (the P.V MMA's accumulator): lane (g = lane/4, c = lane%4) holds, for
 // heads h_e = 2c + e (e = 0, 1) and dims d = 16t + g + 8j, o[t][2j + e].  mh/lh: base-2 running
-// max and the (lane-reduced) sum of the two heads.
+// max and the (lane-reduced) sum of the two heads.  Online over the slots (fixed order: bit-
+// deterministic): a slot's lse and o rows are loaded together, one memory round trip per slot
+// (round 1 loaded all lse first, then the o rows: two).
 template <int D, int G>
 __device__ __forceinline__ void finalize(const SuffixArgs &a, int req, int head, int nslots, int lane,
-                                         const float (&mh)[2], const float (&lh)[2], float (&o)[D / 16][4],
-                                         const float (&lse0)[2], bool have0) {
+                                         const float (&mh)[2], const float (&lh)[2], float (&o)[D / 16][4]) {
     constexpr int KS = D / 16;
     const PlanDev &P = a.p;
     const int g = lane >> 2, c = lane & 3;
     const int64_t slot_stride = (int64_t)P.nreq * a.hq;
     const int64_t row0 = (int64_t)req * a.hq + head * G;
+    // lanes of padding heads (2c + e >= G) read head 0's rows (valid addresses; results unused)
+    const int64_t r0 = row0 + (2 * c < G ? 2 * c : 0), r1 = row0 + (2 * c + 1 < G ? 2 * c + 1 : 0);
+    float xl[2], xo[KS][4];
+    auto load_slot = [&](int sl) {
+        const int64_t s = (int64_t)sl * slot_stride;
+        xl[0] = __ldcg(P.part_lse + s + r0);
+        xl[1] = __ldcg(P.part_lse + s + r1);
+        const float *s0 = P.part_o + (s + r0) * D + g, *s1 = P.part_o + (s + r1) * D + g;
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+            xo[t][0] = __ldcg(s0 + 16 * t);
+            xo[t][2] = __ldcg(s0 + 16 * t + 8);
+            xo[t][1] = __ldcg(s1 + 16 * t);
+            xo[t][3] = __ldcg(s1 + 16 * t + 8);
+        }
+    };
     float M[2], L[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-        const int h = 2 * c + e;
-        M[e] = (lh[e] > 0.f) ? mh[e] + __log2f(lh[e]) : -INFINITY;
-        if (h < G)
-            for (int sl = 0; sl < nslots; ++sl)
-                M[e] = fmaxf(M[e], (sl == 0 && have0 ? lse0[e] : P.part_lse[sl * slot_stride + row0 + h]) * kLog2e);
-        const float ws = (lh[e] > 0.f) ? ptx::ex2(mh[e] - M[e]) : 0.f;
-        L[e] = lh[e] * ws;
-#pragma unroll
-        for (int t = 0; t < KS; ++t) {
-            o[t][e] *= ws;
-            o[t][2 + e] *= ws;
-        }
+        M[e] = lh[e] > 0.f ? mh[e] : -INFINITY;
+        L[e] = lh[e];
     }
     for (int sl = 0; sl < nslots; ++sl) {
+        load_slot(sl);  // lse and o rows of the slot: one round trip
+        float cl[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) cl[e] = xl[e] * kLog2e;
+        float (&co)[KS][4] = xo;
+        float al[2], w[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const int h = 2 * c + e;
-            if (h >= G) continue;
-            const int64_t row = sl * slot_stride + row0 + h;
-            const float w = ptx::ex2((sl == 0 && have0 ? lse0[e] : P.part_lse[row]) * kLog2e - M[e]);
-            L[e] += w;
-            const float *src = P.part_o + row * D + g;
+            const float mn = fmaxf(M[e], cl[e]);
+            al[e] = ptx::ex2(M[e] - mn);  // 0 while M is -inf (no suffix tokens yet)
+            w[e] = ptx::ex2(cl[e] - mn);
+            L[e] = L[e] * al[e] + w[e];
+            M[e] = mn;
+        }
 #pragma unroll
-            for (int t = 0; t < KS; ++t) {
-                o[t][e] = fmaf(w, src[16 * t], o[t][e]);
-                o[t][2 + e] = fmaf(w, src[16 * t + 8], o[t][2 + e]);
-            }
+        for (int t = 0; t < KS; ++t) {
+            o[t][0] = fmaf(w[0], co[t][0], o[t][0] * al[0]);
+            o[t][2] = fmaf(w[0], co[t][2], o[t][2] * al[0]);
+            o[t][1] = fmaf(w[1], co[t][1], o[t][1] * al[1]);
+            o[t][3] = fmaf(w[1], co[t][3], o[t][3] * al[1]);
         }
     }
 #pragma unroll
@@ -354,60 +373,78 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
     int32_t *plist = reinterpret_cast<int32_t *>(ms + S::OFF_PARK);
     int npark = 0;
     // has K1 finished (all its CTAs published)?  A hint only: outputs are written after
-    // griddepcontrol.wait either way.
+    // griddepcontrol.wait either way.  Lane 0 polls the completion counter once per block with
+    // a non-blocking load whose value is read one block later, so the unit ends find the
+    // answer without a round trip.
+    uint32_t k1_poll = 0;     // lane 0: the last poll (possibly still in flight)
+    bool k1_polled = false, k1_seen = false;
+    auto k1_poll_issue = [&]() {
+        if (lane == 0) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(k1_poll) : "l"(P.k1_done + ls));
+        k1_polled = true;
+    };
+    auto k1_poll_check = [&]() {
+        if (!k1_ready && !k1_seen && k1_polled && __shfl_sync(0xffffffffu, k1_poll, 0) >= (uint32_t)P.ntiles)
+            k1_seen = true;
+    };
     auto k1_hint = [&]() -> bool {
-        if (k1_ready) return true;
+        if (k1_ready || k1_seen) return true;
+        if (k1_polled) {
+            k1_poll_check();
+            return k1_seen;
+        }
         uint32_t v = 0;
         if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.k1_done + ls) : "memory");
         v = __shfl_sync(0xffffffffu, v, 0);
         return v >= (uint32_t)P.ntiles;
     };
-    // merge every stream-K piece of unit u (in segment order: deterministic) and finalize
+    // merge every stream-K piece of unit u (in segment order: deterministic) and finalize;
+    // online over the pieces, each piece's (m, l) and o loaded together
     auto merge_pieces = [&](int u) {
         const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
         const int req = m0.z, head = m0.w, nslots = m1.x, nseg = m1.y, base = m1.z;
-        float lseM[2] = {0.f, 0.f};
-        const bool haveM = nslots > 0;
-        if (haveM) {
-            const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
+        const int c2 = 2 * c < G ? 2 * c : 0;  // padding-head lanes read head 0 (results unused)
+        float2 xml[2];
+        float4 xo[KS];
+        auto load_seg = [&](int sg) {
+            const int64_t sidx = base + sg;
 #pragma unroll
             for (int e = 0; e < 2; ++e)
-                if (2 * c + e < G) lseM[e] = __ldcg(src + 2 * c + e);
-        }
+                xml[e] = __ldcg(reinterpret_cast<const float2 *>(seg_ml + (sidx * NPAD + (2 * c + e < G ? 2 * c + e : c2)) * 2));
+            const float *src = seg_o + sidx * (NPAD * D) + (2 * c < G ? lane : 0) * (4 * KS);
+#pragma unroll
+            for (int t = 0; t < KS; ++t) xo[t] = __ldcg(reinterpret_cast<const float4 *>(src + 4 * t));
+        };
         float M[2] = {-INFINITY, -INFINITY}, L[2] = {0.f, 0.f};
         float o[KS][4];
 #pragma unroll
         for (int t = 0; t < KS; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-        if (2 * c < G) {
-            for (int sg = 0; sg < nseg; ++sg)
+        for (int sg = 0; sg < nseg; ++sg) {
+            load_seg(sg);  // the piece's (m, l) and o: one round trip
+            const float2 (&cml)[2] = xml;
+            const float4 (&co)[KS] = xo;
+            float al[2], w[2];
 #pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    if (2 * c + e < G)
-                        M[e] = fmaxf(M[e], __ldcg(seg_ml + ((int64_t)(base + sg) * NPAD + 2 * c + e) * 2));
-            for (int sg = 0; sg < nseg; ++sg) {
-                float w[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
+            for (int e = 0; e < 2; ++e) {
+                if (cml[e].y > 0.f) {  // a piece with tokens (l > 0): fold it in
+                    const float mn = fmaxf(M[e], cml[e].x);
+                    al[e] = ptx::ex2(M[e] - mn);
+                    w[e] = ptx::ex2(cml[e].x - mn);
+                    L[e] = L[e] * al[e] + cml[e].y * w[e];
+                    M[e] = mn;
+                } else {
+                    al[e] = 1.f;
                     w[e] = 0.f;
-                    if (2 * c + e < G) {
-                        const float2 ml = __ldcg(reinterpret_cast<const float2 *>(
-                            seg_ml + ((int64_t)(base + sg) * NPAD + 2 * c + e) * 2));
-                        w[e] = (ml.y > 0.f) ? ptx::ex2(ml.x - M[e]) : 0.f;
-                        L[e] += ml.y * w[e];
-                    }
-                }
-                const float *src = seg_o + (int64_t)(base + sg) * (NPAD * D) + lane * (4 * KS);
-#pragma unroll
-                for (int t = 0; t < KS; ++t) {
-                    const float4 x = __ldcg(reinterpret_cast<const float4 *>(src + 4 * t));
-                    o[t][0] = fmaf(w[0], x.x, o[t][0]);
-                    o[t][1] = fmaf(w[1], x.y, o[t][1]);
-                    o[t][2] = fmaf(w[0], x.z, o[t][2]);
-                    o[t][3] = fmaf(w[1], x.w, o[t][3]);
                 }
             }
+#pragma unroll
+            for (int t = 0; t < KS; ++t) {
+                o[t][0] = fmaf(w[0], co[t].x, o[t][0] * al[0]);
+                o[t][1] = fmaf(w[1], co[t].y, o[t][1] * al[1]);
+                o[t][2] = fmaf(w[0], co[t].z, o[t][2] * al[0]);
+                o[t][3] = fmaf(w[1], co[t].w, o[t][3] * al[1]);
+            }
         }
-        finalize<D, G>(a, req, head, nslots, lane, M, L, o, lseM, haveM);
+        finalize<D, G>(a, req, head, nslots, lane, M, L, o);
     };
     // wait for K1, then merge the parked units (whole units from `park`, stream-K ones from
     // their pieces) in parking order
@@ -439,8 +476,7 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
                 mm[e] = ml.x;
                 ll[e] = ml.y;
             }
-            const float z[2] = {0.f, 0.f};
-            finalize<D, G>(a, m0.z, m0.w, m1.x, lane, mm, ll, o, z, false);
+            finalize<D, G>(a, m0.z, m0.w, m1.x, lane, mm, ll, o);
         }
         __syncwarp();
         npark = 0;
@@ -471,16 +507,6 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
             const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
             const int xs = max(m0.x, lo), xe = min(m0.y, hi);
             const int req = m0.z, head = m0.w;
-            // once K1 is known complete, the merge's first partial lse is loaded now and
-            // lands while the unit streams (the merge otherwise waits one L2 round trip)
-            float lse0[2] = {0.f, 0.f};
-            const bool have0 = k1_ready && m1.x > 0 && m1.y == 1;
-            if (have0) {
-                const float *src = P.part_lse + (int64_t)req * a.hq + head * G;
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    if (2 * c + e < G) lse0[e] = __ldcg(src + 2 * c + e);
-            }
             // O^T accumulators (d x 8 heads, MMA C layout), running max / lane-partial sums
             float o[KS][4];
 #pragma unroll
@@ -502,11 +528,17 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
 
                 for (int x = xs; x < xe; ++x) {
                     fill();
+                    if (!k1_ready && !k1_seen) {  // refresh the K1 completion hint
+                        k1_poll_check();
+                        if (!k1_seen) k1_poll_issue();
+                    }
                     const int st = c_count % ST;
                     ptx::mbar_wait(&full[st], (c_count / ST) & 1);
 #ifdef HALO_K2_TRACE
                     if (c_count == 0) K2_TRACE(gw, 1);
+                    K2_TRACE(gw, 4);
 #endif
+                    if (HALO_K2_EXP & 1) { __syncwarp(); ++c_count; continue; }
                     const int ntok = snt[st];
                     const uint32_t kb = ptx::smem_u32(stages + st * S::STAGE);
                     const uint32_t vb = kb + S::SLAB;
@@ -600,10 +632,12 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
                 l[1] += __shfl_xor_sync(0xffffffffu, l[1], msk);
             }
             const int nslots = m1.x, nseg = m1.y;
+            K2_TRACE(gw, 5);
+            if (HALO_K2_EXP & 2) { __syncwarp(); continue; }
             if (nseg == 1) {
                 if (k1_hint()) {
                     wait_k1();  // first output write of this grid: K1 (and before it the previous K2) done
-                    finalize<D, G>(a, req, head, nslots, lane, m, l, o, lse0, have0);
+                    finalize<D, G>(a, req, head, nslots, lane, m, l, o);
                 } else {
                     // K1 still runs: park the unit's state (L2) and stream on; merged by drain()
                     float *pk = park + (int64_t)u * PARK_UNIT;
@@ -661,6 +695,7 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
         }
     }
     if (npark > 0) drain();
+    K2_TRACE(gw, 6);
     // the launch's last warp resets this layer slot's completion hints
     __syncwarp();
     if (lane == 0) {

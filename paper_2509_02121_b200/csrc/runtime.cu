@@ -884,6 +884,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         };
         std::vector<int64_t> cuts;
         bool bal = false;
+        const bool few_units = U > Ww && U <= 3 * Wn;  // 1-3 whole units per narrow warp
         if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
             cuts.assign(1, 0);
             for (int64_t x = pl->opt.k2_chunk_blocks; x < Itot; x += pl->opt.k2_chunk_blocks) push_cut(cuts, x);
@@ -893,10 +894,14 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             cuts = equal_cuts(Wn, kK2WarpsNarrow);
         } else if (pl->opt.k2_shape == 1) {  // forced wide shape
             cuts = equal_cuts(Ww, kK2WarpsWide);
-        } else if (Btot < 8 * (int64_t)U && U < 2 * Ww &&
+        } else if (((Btot < 8 * (int64_t)U && U < 2 * Ww) || (ew == 1.0 && few_units)) &&
                    (cuts = snapped_cuts(Wn, kK2WarpsNarrow, bal), bal)) {
-            // few units per warp (stream-K pieces would dominate) and whole units divide
-            // evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces
+            // few units per warp (stream-K pieces would dominate: C1 has 1.15 units per wide
+            // warp, so nearly every unit would be cut in two, and each merge costs the piece
+            // that finishes last several memory round trips at the end of the kernel) and whole
+            // units divide evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces.
+            // Beside K1 (co-schedule weights) the wide shape with pieces measured faster
+            // (C1: 53.6 vs 59.9 us per layer, profiles/k2_narrow_r02.txt).
             pl->k2_warps = kK2WarpsNarrow;
         } else {
             cuts = snapped_cuts(Ww, kK2WarpsWide, bal);
@@ -996,11 +1001,21 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         // K2 bit) runs without the co-schedule's early-CTA weights: an equal-share schedule
         pl->alt_nchunks = 0;
         pl->alt_nseg_total = 0;
-        if (ew != 1.0 && pl->k2_warps == kK2WarpsWide && pl->dyn_first == (int32_t)nchunks) {
+        pl->alt_k2_warps = pl->k2_warps;
+        if (ew != 1.0 && pl->dyn_first == (int32_t)nchunks) {
             ew = 1.0;
             bool bal2 = false;
-            std::vector<int64_t> ce = snapped_cuts(Ww, kK2WarpsWide, bal2);
-            if (!bal2) ce = equal_cuts(Ww, kK2WarpsWide);
+            // alone, a few whole units per warp over the narrow shape beat stream-K pieces
+            // (C1 K2: 0.83 vs 0.75 of HBM, no merges at the kernel's end)
+            std::vector<int64_t> ce;
+            if (few_units && pl->opt.k2_shape == 0 && pl->opt.k2_chunk_blocks <= 0 &&
+                (ce = snapped_cuts(Wn, kK2WarpsNarrow, bal2), bal2)) {
+                pl->alt_k2_warps = kK2WarpsNarrow;
+            } else {
+                const int64_t Wk = (int64_t)k2_sms(pl) * pl->k2_warps;
+                ce = snapped_cuts(Wk, pl->k2_warps, bal2);
+                if (!bal2) ce = equal_cuts(Wk, pl->k2_warps);
+            }
             if (ce.size() < 2) ce = {0, Itot};
             const int64_t ne = (int64_t)ce.size() - 1;
             fill_cmap(ce);
@@ -1044,6 +1059,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     inf.k1_tiles = (int32_t)pl->tiles.size();
     inf.k2_units = nreq * hkv;
     inf.max_slots = max_slots;
+    inf.k2_warps = pl->k2_warps;
     inf.k1_flops = k1_flops;
     inf.k1_bytes = k1_bytes;
     inf.k2_bytes = k2_bytes;
@@ -1239,6 +1255,8 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
     if (mask & 2) {
         PlanDev dv = pl->dev;
         if (!(mask & 1) && dv.alt_nchunks > 0) {  // K2 alone: the equal-share schedule
+            dv.k2_warps = pl->alt_k2_warps;
+            dv.nwarps = k2_sms(pl) * pl->alt_k2_warps;
             dv.chunk_info = dv.alt_chunk_info;
             dv.unit_meta = dv.alt_unit_meta;
             dv.nchunks = dv.alt_nchunks;

@@ -154,6 +154,7 @@ struct halo_plan_s {
     std::vector<int32_t> alt_chunk_info, alt_unit_meta;
     std::vector<int32_t> item_unit, item_chunk;  // planner scratch (item -> unit / chunk maps)
     int32_t alt_nchunks = 0, alt_nseg_total = 0;
+    int32_t alt_k2_warps = 0;  // launch shape of the K2-alone schedule
     int32_t k2_warps = halo::kK2WarpsWide;
     bool k2_early = false;  // K1 split count lowered so K2's first CTAs stream beside K1
     double k2_early_w = 1.0;  // the co-schedule model's work weight of those CTAs

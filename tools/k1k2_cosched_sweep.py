@@ -41,10 +41,11 @@ def main():
         opt = PlanOptions(0, 0, s, 0)
         opt.k1_sm_frac = -1.0
         opt.k2_early_weight = w
+        opt.k2_shape = int(os.environ.get("K2_SHAPE", "0"))  # 0 planner, 1 wide, 2 narrow
         plan = ld.pool.plan(ld.req_ids, opt)
         info = plan.info()
         ms = timed(lambda: [plan.run(l, q[l], out) for l in range(L)]) / L
-        print(f"{os.path.basename(halo.lib_path())} splits={s} w={w:4.1f} k1_tiles={info['k1_tiles']:4d}: {ms * 1e3:6.1f} us/layer "
+        print(f"{os.path.basename(halo.lib_path())} shape={info.get('k2_warps', '?')} splits={s} w={w:4.1f} k1_tiles={info['k1_tiles']:4d}: {ms * 1e3:6.1f} us/layer "
               f"{wl.nreq / ms * 1e3 / 1e6:6.3f} M q/s", flush=True)
         plan.destroy()
     ld.pool.destroy()

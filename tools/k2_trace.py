@@ -1,5 +1,6 @@
 """Per-warp timeline of K2 (debug build with -DHALO_K2_TRACE): entry, first K/V stage
-landed, K1 complete (griddepcontrol.wait returned), exit -- in us from the earliest entry.
+landed, K1 complete (griddepcontrol.wait returned), last K/V stage landed, start of the last
+unit end (merge / finalize / publish), exit -- in us from the earliest entry.
 
 Two runs on the chosen config (CFG=fanout|tree|analytics, LAYERS):
   alone : K2 by itself after an L2 flush (K1's partials already written)
@@ -48,7 +49,7 @@ def main():
     lib = halo.load_library()
     lib.halo_debug_k2_trace.argtypes = [ctypes.c_void_p]
     W = 148 * 16
-    buf = torch.zeros(W * 4, dtype=torch.int64, device="cuda:0")
+    buf = torch.zeros(W * 8, dtype=torch.int64, device="cuda:0")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda:0")
     print(f"{cfg}: k1_tiles={info['k1_tiles']} k2_units={info['k2_units']} k2_bytes={info['k2_bytes']:.3e}")
     for mode in ("alone", "pdl"):
@@ -61,7 +62,7 @@ def main():
             plan.run_stages(1, 2 if mode == "alone" else 3, q[1], out)
             lib.halo_debug_k2_trace(ctypes.c_void_p(0))
             torch.cuda.synchronize()
-        t = buf.view(W, 4).cpu().numpy().astype(np.float64)
+        t = buf.view(W, 8).cpu().numpy().astype(np.float64)
         used = t[:, 0] > 0
         t = t[used]
         t[t == 0] = np.nan
@@ -70,8 +71,13 @@ def main():
         span = np.nanmax(t[:, 3])
         print(f"-- {mode}: warps={used.sum()} span={span:.2f} us  "
               f"(k2 bytes / span = {info['k2_bytes'] / span / 1e3:.0f} GB/s)")
-        for name, col in [("entry", 0), ("first data", 1), ("k1 done", 2), ("exit", 3)]:
+        for name, col in [("entry", 0), ("first data", 1), ("k1 done", 2), ("last data", 4),
+                          ("last unit end", 5), ("exit", 3)]:
             print(stats(name, t[:, col]))
+        print(stats("end latency", t[:, 3] - t[:, 5]))
+        print(stats("unit end", t[:, 6] - t[:, 5]))
+        print(stats("final atomic", t[:, 3] - t[:, 6]))
+        print(stats("tail after data", t[:, 3] - t[:, 4]))
         print(stats("busy", t[:, 3] - t[:, 0]))
         ncta_warps = int(os.environ.get("K2_WARPS", "0")) or None
         if ncta_warps:

@@ -53,8 +53,12 @@ def launches(path):
     hdr, data = rows[hi], rows[hi + 1:]
     ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     agg = defaultdict(list)
+    seen_step = False  # launches before the first K1 are the one-time load (registration)
     for r in data:
         name = r[ik].split("(")[0].split("<")[0].split("::")[-1]
+        seen_step = seen_step or name.startswith("prefix_attn")
+        if not seen_step:
+            name += " (load, one-time)"
         v = float(r[iv].replace(",", ""))
         scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[iu], 1e-3)
         agg[name].append(v * scale)
@@ -87,10 +91,13 @@ def main():
                          "report": os.path.basename(rep), "round": tag}
     if lcsv:
         agg = launches(lcsv)
-        tot = sum(sum(v) for v in agg.values())
-        md.append("\n## launch list (`ncu --metrics gpu__time_duration.sum`)\n\n| kernel | launches | mean us | share |\n|---|---|---|---|")
+        tot = sum(sum(v) for k, v in agg.items() if "one-time" not in k)  # share of the steps
+        md.append("\n## launch list (`ncu --metrics gpu__time_duration.sum`)\n\nShare = of the decode steps' "
+                  "kernel time (the one-time load launches are listed, not counted).\n\n"
+                  "| kernel | launches | mean us | share |\n|---|---|---|---|")
         for n, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-            md.append(f"| {n} | {len(v)} | {sum(v)/len(v):.2f} | {100*sum(v)/tot:.1f}% |")
+            share = "-" if "one-time" in n else f"{100*sum(v)/tot:.1f}%"
+            md.append(f"| {n} | {len(v)} | {sum(v)/len(v):.2f} | {share} |")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w").write("\n".join(md) + "\n")
     tp = os.path.join(ROOT, "profiles", "traffic.json")

@@ -894,14 +894,15 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             cuts = equal_cuts(Wn, kK2WarpsNarrow);
         } else if (pl->opt.k2_shape == 1) {  // forced wide shape
             cuts = equal_cuts(Ww, kK2WarpsWide);
-        } else if (((Btot < 8 * (int64_t)U && U < 2 * Ww) || (ew == 1.0 && few_units)) &&
+        } else if (((Btot < 8 * (int64_t)U && U < 2 * Ww) || (k1c == 0 && few_units)) &&
                    (cuts = snapped_cuts(Wn, kK2WarpsNarrow, bal), bal)) {
             // few units per warp (stream-K pieces would dominate: C1 has 1.15 units per wide
             // warp, so nearly every unit would be cut in two, and each merge costs the piece
             // that finishes last several memory round trips at the end of the kernel) and whole
             // units divide evenly over the narrow shape: 7 warps x 4 stages per SM, no pieces.
-            // Beside K1 (co-schedule weights) the wide shape with pieces measured faster
-            // (C1: 53.6 vs 59.9 us per layer, profiles/k2_narrow_r02.txt).
+            // Only without K1 in the plan: beside K1 (under PDL) the wide shape with pieces
+            // measured faster (C1: 53.6 vs 59.9 us per layer, profiles/k2_narrow_r02.txt);
+            // such plans get the whole-unit schedule for K2 launched alone (below).
             pl->k2_warps = kK2WarpsNarrow;
         } else {
             cuts = snapped_cuts(Ww, kK2WarpsWide, bal);

@@ -468,8 +468,8 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             }
             float mxv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int i = 0; i < kK1Tok; i += 2)
-                mxv[(i >> 1) & 3] = fmaxf(mxv[(i >> 1) & 3], fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+            for (int i = 0; i < kK1Tok; i += 2)  // 3-input max (FMNMX3): one instruction per pair
+                asm("max.f32 %0, %0, %1, %2;" : "+f"(mxv[(i >> 1) & 3]) : "f"(__uint_as_float(sr[i])), "f"(__uint_as_float(sr[i + 1])));
             const float mx = fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3]));
             if (threadIdx.x == 0) K1_TRACE_DEP(10, n, mx);
             // lazy reference max: move it (and rescale O) only when a row's max grew by > 2^8

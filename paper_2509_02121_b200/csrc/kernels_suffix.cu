@@ -399,13 +399,22 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
     };
     // merge every stream-K piece of unit u (in segment order: deterministic) and finalize;
     // online over the pieces, each piece's (m, l) and o loaded together
-    auto merge_pieces = [&](int u) {
+    // `own` >= 0: this warp's piece of the unit, whose state (om, ol, oo) is still in registers
+    // (not re-read from L2: one round trip less at the end of the kernel)
+    auto merge_pieces = [&](int u, int own, const float (&om)[2], const float (&ol)[2], const float (&oo)[KS][4]) {
         const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
         const int req = m0.z, head = m0.w, nslots = m1.x, nseg = m1.y, base = m1.z;
         const int c2 = 2 * c < G ? 2 * c : 0;  // padding-head lanes read head 0 (results unused)
         float2 xml[2];
         float4 xo[KS];
         auto load_seg = [&](int sg) {
+            if (sg == own) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) xml[e] = make_float2(om[e], ol[e]);
+#pragma unroll
+                for (int t = 0; t < KS; ++t) xo[t] = make_float4(oo[t][0], oo[t][1], oo[t][2], oo[t][3]);
+                return;
+            }
             const int64_t sidx = base + sg;
 #pragma unroll
             for (int e = 0; e < 2; ++e)
@@ -451,11 +460,12 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
     auto drain = [&]() {
         wait_k1();
         __syncwarp();
+        const float zm[2] = {0.f, 0.f}, zo[KS][4] = {};  // (parked pieces: all state in L2)
         for (int i = 0; i < npark; ++i) {
             const int ent = plist[i];
             const int u = ent & 0x7fffffff;
             if (ent < 0) {
-                merge_pieces(u);
+                merge_pieces(u, -1, zm, zm, zo);
                 continue;
             }
             const int4 m0 = P.unit_meta[2 * u], m1 = P.unit_meta[2 * u + 1];
@@ -683,7 +693,7 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
                     if (lane == 0) unit_count[u] = 0;  // ready for this slot's next launch
                     if (k1_hint()) {
                         wait_k1();
-                        merge_pieces(u);
+                        merge_pieces(u, cc - m1.w, m, l, o);
                     } else {
                         if (lane == 0) plist[npark] = u | (int)0x80000000;
                         ++npark;

@@ -667,37 +667,74 @@ suffix_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_const
                     if (npark == NPARK) drain();
                 }
             } else {
-                // ---- stream-K: publish this piece's state; the last piece merges them all ----
-                const int slot = m1.z + (cc - m1.w);
-                float *so = seg_o + (int64_t)slot * (NPAD * D) + lane * (4 * KS);
-                if (2 * c < G) {
+                // ---- stream-K piece ----
+                // Static schedules with one chunk per warp: the unit's FIRST piece (segment 0 --
+                // always the last unit of its chunk, so every other piece sits at the start or
+                // middle of another warp's chunk and never waits) merges: the other pieces
+                // publish and arrive without a return value, the merger waits for their count
+                // with an acquire poll and folds its own state from registers (no publish, no
+                // arrival round trip).  Otherwise the last piece to arrive merges.
+                const int own = cc - m1.w;
+                const bool designated = !dyn && P.nchunks <= P.nwarps;
+                auto publish = [&]() {
+                    const int slot = m1.z + own;
+                    float *so = seg_o + (int64_t)slot * (NPAD * D) + lane * (4 * KS);
+                    if (2 * c < G) {
 #pragma unroll
-                    for (int t = 0; t < KS; ++t) *reinterpret_cast<float4 *>(so + 4 * t) = make_float4(o[t][0], o[t][1], o[t][2], o[t][3]);
-                }
-                if (g == 0) {
+                        for (int t = 0; t < KS; ++t) *reinterpret_cast<float4 *>(so + 4 * t) = make_float4(o[t][0], o[t][1], o[t][2], o[t][3]);
+                    }
+                    if (g == 0) {
 #pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        if (2 * c + e < G)
-                            *reinterpret_cast<float2 *>(seg_ml + ((int64_t)slot * NPAD + 2 * c + e) * 2) = make_float2(m[e], l[e]);
-                }
-                // one acq_rel arrival by lane 0: release covers the whole warp's stores
-                // (ordered before it by the warp barrier), acquire makes the other pieces'
-                // stores visible to the merging warp (read from L2 with ld.cg)
-                __syncwarp();
-                int old = 0;
-                if (lane == 0)
-                    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                                 : "=r"(old) : "l"(unit_count + u) : "memory");
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == nseg - 1) {
-                    if (lane == 0) unit_count[u] = 0;  // ready for this slot's next launch
+                        for (int e = 0; e < 2; ++e)
+                            if (2 * c + e < G)
+                                *reinterpret_cast<float2 *>(seg_ml + ((int64_t)slot * NPAD + 2 * c + e) * 2) = make_float2(m[e], l[e]);
+                    }
+                    __syncwarp();  // the warp's stores before lane 0's release
+                };
+                if (designated && own == 0) {
+                    if (lane == 0) {  // the other pieces' arrivals (release): acquire
+                        uint32_t v;
+                        for (;;) {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(unit_count + u) : "memory");
+                            if (v >= (uint32_t)(nseg - 1)) break;
+                            __nanosleep(100);
+                        }
+                        unit_count[u] = 0;  // ready for this slot's next launch
+                    }
+                    __syncwarp();
                     if (k1_hint()) {
                         wait_k1();
-                        merge_pieces(u, cc - m1.w, m, l, o);
-                    } else {
+                        merge_pieces(u, own, m, l, o);
+                    } else {  // K1 still runs: publish the own piece too and merge in drain()
+                        publish();
                         if (lane == 0) plist[npark] = u | (int)0x80000000;
                         ++npark;
                         if (npark == NPARK) drain();
+                    }
+                } else if (designated) {
+                    publish();
+                    if (lane == 0)
+                        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(unit_count + u) : "memory");
+                } else {
+                    // one acq_rel arrival by lane 0: release covers the whole warp's stores
+                    // (ordered before it by the warp barrier), acquire makes the other pieces'
+                    // stores visible to the merging warp (read from L2 with ld.cg)
+                    publish();
+                    int old = 0;
+                    if (lane == 0)
+                        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                                     : "=r"(old) : "l"(unit_count + u) : "memory");
+                    old = __shfl_sync(0xffffffffu, old, 0);
+                    if (old == nseg - 1) {
+                        if (lane == 0) unit_count[u] = 0;  // ready for this slot's next launch
+                        if (k1_hint()) {
+                            wait_k1();
+                            merge_pieces(u, own, m, l, o);
+                        } else {
+                            if (lane == 0) plist[npark] = u | (int)0x80000000;
+                            ++npark;
+                            if (npark == NPARK) drain();
+                        }
                     }
                 }
             }

@@ -11,8 +11,9 @@
 // B200 design:
 //  * static schedule: the (request, kv head) units' blocks form one sequence, cut by the
 //    planner into equal contiguous chunks, one per warp (148 SMs x 12 or 7 warps).  A unit cut
-//    by chunk boundaries leaves one partial softmax state per piece; the last piece to
-//    finish (atomic arrival counter) merges them in a fixed order -> bit-deterministic.
+//    by chunk boundaries leaves one partial softmax state per piece; the unit's first piece
+//    (the last unit of its chunk) merges them once the others have arrived (otherwise the
+//    last piece to arrive does), in a fixed order -> bit-deterministic.
 //  * warp-level streaming: every warp owns a ring of 2 (or 4) smem stages; its lane 0
 //    issues one 1-D bulk async copy (cp.async.bulk, TMA engine) per 4-KiB K slab and V
 //    slab of a 16-token block, completion on a per-stage mbarrier.  The unit's g query

@@ -215,6 +215,11 @@ def setup_workload(halo, wl, dev, torch):
         pool.truncate(reqs, ones)                 # stationary batch: roll back, re-append
         pool.append(reqs, ones, nk, nv)
         pool.plan(reqs, popt, reuse=plan)
+        if evs is not None:
+            # breakdown pass: hold the stream (a ~3 ms spin kernel, outside every event pair)
+            # while the host enqueues the step's 32 x (event, K1, event, K2, event), so no
+            # interval between two events contains host enqueue latency
+            torch.cuda._sleep(6_000_000)
         for l in range(L):
             if evs is None:                       # headline pass: K1 -> K2 back to back (PDL)
                 plan.run(l, q[l], out[l], lse[l])
@@ -234,8 +239,10 @@ def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=Fa
          programmatic dependent launch overlaps K1's tail);
       2. the breakdown pass: an event before K1, between K1 and K2 and after K2 of every
          layer (per-kernel launch durations for the rooflines; the events serialise the
-         kernels, so this pass is a little slower than the first).
-    Returns (pass-1 ms, pass-2 ms, pass-2 K1 ms, pass-2 K2 ms, clock sampler)."""
+         kernels, so this pass is a little slower than the first).  Each step's layers are
+         enqueued behind a spin kernel, so no event interval holds host enqueue latency.
+    Returns (pass-1 ms, pass-2 ms of the steps' layer spans, pass-2 K1 ms, pass-2 K2 ms,
+    clock sampler)."""
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         step()
@@ -264,7 +271,8 @@ def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=Fa
             dist.barrier()
     if clk:
         clk.__exit__()
-    ms, ms_bd = t[0].elapsed_time(t[1]), t[2].elapsed_time(t[3])
+    ms = t[0].elapsed_time(t[1])
+    ms_bd = sum(st[0][0].elapsed_time(st[L - 1][2]) for st in evs)  # first K1 .. last K2
     per_step = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(steps))
     time_steps.step_stats = {"median": per_step[len(per_step) // 2],
                              "p90": per_step[min(len(per_step) - 1, (9 * len(per_step)) // 10)],
@@ -556,9 +564,9 @@ def main():
         except Exception as e:  # noqa: BLE001
             extra[key] = {"error": f"{type(e).__name__}: {e}"}
             torch.cuda.synchronize()
-    # ---- K2 with equal per-warp shares (the co-schedule weights off, same K1 splits): the
-    # kernel's own capability; the breakdown pass above runs K2 alone with the weights the
-    # planner set for running BESIDE K1, which leaves it imbalanced by design ----
+    # ---- K2 alone with the wide stream-K schedule and equal per-warp shares (co-schedule
+    # weights off, same K1 splits), for comparison: the breakdown pass above runs K2 alone
+    # with the plan's K2-alone schedule (C1: whole units over the narrow shape) ----
     if not args.profile:
         def k2_equal():
             eopt = halo.PlanOptions(0, 0, int(os.environ.get("HALO_MAX_SPLITS", "0")), 0)
@@ -567,6 +575,8 @@ def main():
             einfo = ep.info()
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
             for rep in range(4):
+                if rep == 3:
+                    torch.cuda._sleep(6_000_000)  # the timed layers enqueued behind a spin kernel
                 for l in range(L):
                     ep.run_stages(l, 1, q[l], out[l], lse[l])
                     if rep == 3:
@@ -578,7 +588,8 @@ def main():
             k2ms = sum(a.elapsed_time(b) for a, b in evs) / L
             ep.destroy()
             r = kernel_rooflines(einfo, k1_launch_ms, k2ms)[0]
-            r["timing"] = "CUDA events around each K2 launch (K1 before it, serialised), 32 layers"
+            r["timing"] = ("CUDA events around each K2 launch (K1 before it, serialised), 32 layers; "
+                           "wide shape, stream-K pieces, equal shares")
             return r
         guarded("roofline_k2_equal_shares", k2_equal)
         hbm_peak = peaks()[0]
@@ -677,10 +688,11 @@ def main():
             "roofline": dict(k2_roof, traffic=traffic),
             "prefix_roofline": k1_roof,
             "step_ms_distribution": step_stats,
-            "step_breakdown_ms": {"pass": "breakdown pass (events around each kernel)",
-                                  "step": ms_bd / args.steps, "k1": k1_ms / args.steps,
+            "step_breakdown_ms": {"pass": "breakdown pass (events around each kernel; K1 and K2 "
+                                          "serialised; append + plan not included)",
+                                  "layers": ms_bd / args.steps, "k1": k1_ms / args.steps,
                                   "k2": k2_ms / args.steps,
-                                  "other": (ms_bd - k1_ms - k2_ms) / args.steps},
+                                  "gaps": (ms_bd - k1_ms - k2_ms) / args.steps},
             "unshared_bytes_per_layer": info["unshared_bytes"],
             "gpu_launches": launches,
             "clocks": clk.summary(),

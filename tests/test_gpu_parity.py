@@ -581,3 +581,23 @@ def test_k2_alone_uses_the_equal_share_schedule_and_matches_oracle():
     for o in (o1, o2):
         assert np.abs(o.cpu().numpy()[::5] - ro).max() <= OUT_TOL
     cleanup(ld, plan)
+
+
+def test_stream_k_pieces_beside_a_long_k1_park_and_merge():
+    """Units cut into several stream-K pieces (64 requests x 8 kv heads = 512 units of 17
+    blocks for ~1776 warps) while K1 runs long (an 8k-token prefix): the unit's first piece
+    merges once the other pieces arrived, parking its state when K1 is still running (merged
+    after griddepcontrol.wait); two layers, every request vs the oracle, and a rerun of the
+    same plan is bit-identical."""
+    wl = make_config("fanout", layers=2, nreq=64, prefix=8192, suffix=255)
+    ld, plan, out, lse = run_step(wl)
+    for l in range(2):
+        ro, rl = oracle.decode_reference(wl, l, steps=1)
+        assert np.abs(out[l] - ro).max() <= OUT_TOL and np.abs(lse[l] - rl).max() <= LSE_TOL
+    q = wl.q(0, f"cuda:{DEV}")
+    o2 = torch.empty((wl.nreq, wl.hq, wl.d), device=f"cuda:{DEV}")
+    l2 = torch.empty((wl.nreq, wl.hq), device=f"cuda:{DEV}")
+    plan.run(1, q[1], o2, l2)
+    torch.cuda.synchronize()
+    assert np.array_equal(o2.cpu().numpy(), out[1]) and np.array_equal(l2.cpu().numpy(), lse[1])
+    cleanup(ld, plan)

@@ -568,12 +568,15 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         // get w = (r_e T1 + r_pe T2) / (r_pl T2) times a late CTA's share (T2 = T - T1; CTAs
         // already streaming keep more of the bandwidth after K1 than the ones entering then).
         // Constants measured on B200 (round 2: tools/k1k2_cosched_sweep.py, tools/k2_trace.py,
-        // profiles/k1k2_cosched_r02b.txt, k2_trace_cosched_r02.txt).
+        // profiles/k1k2_cosched_r02b.txt, k2_trace_cosched_r02.txt); r_pe and r_pl re-measured
+        // on the session-3 K2 (cheaper unit ends): PDL trace at w = 3.0, balanced (early / late
+        // CTAs exit at 55.6 / 54.8 us): late CTAs 0.90 MB in 30.5 us = 29 GB/s, early CTAs
+        // 2.69 MB = 44 x 24.3 + r_pe x 31.3 -> 52 GB/s (profiles/k2_trace_w3_r02.txt).
         pl->k2_early = false;
         pl->k2_early_w = 1.0;
         if (k1_sm_frac(pl) > 0 && pl->opt.max_splits <= 0) {
             constexpr double kT0 = 3.0, kTn = 2.75;          // us: K1 CTA prologue+epilogue, per n-tile
-            constexpr double kRe = 44e3, kRpe = 56e3, kRpl = 23e3;  // bytes/us per SM: beside K1, after K1
+            constexpr double kRe = 44e3, kRpe = 52e3, kRpl = 29e3;  // bytes/us per SM: beside K1, after K1
             constexpr double kR = 6.2e6;                     // bytes/us: HBM, K2 streaming on all SMs
             auto tiles_for = [&](int64_t Cc, int64_t &max_ch) {
                 int64_t T = 0;

@@ -28,7 +28,7 @@ def timed(fn, reps=20):
 
 def main():
     halo.load_library()
-    L = 8
+    L = int(os.environ.get("LAYERS", "8"))
     wl = make_config(os.environ.get("CFG", "fanout"), layers=L)
     ld = load(wl, 0)
     append_step(ld, wl, 0, 0)

@@ -119,6 +119,9 @@ cudaError_t launch_prefix_attn(const CUtensorMap *tmap_k, const CUtensorMap *tma
                                int layer, const void *q, float scale, cudaStream_t s);
 // K2+K3: paged-suffix decode with the fused log-sum-exp merge of the K1 partials.  K/V slabs
 // arrive by TMA through the pool's one-block tensor maps (tmap_k / tmap_v, 128-B swizzle).
+// K3 alone (plans with no K2 blocks: every row a merge of its K1 partials).
+cudaError_t launch_merge_only(const PlanDev &p, const PoolGeom &g, int layer, float *out, float *lse,
+                              cudaStream_t s);
 cudaError_t launch_suffix_decode(const CUtensorMap *tmap_k, const CUtensorMap *tmap_v, const PlanDev &p,
                                  const PoolGeom &g, int layer, const void *q, float *out, float *lse,
                                  float scale, cudaStream_t s);

@@ -812,3 +812,107 @@ cudaError_t launch_suffix_decode(const CUtensorMap *tmap_k, const CUtensorMap *t
 }
 
 }  // namespace halo
+
+// ---------------------------------------------------------------------------------------
+// K3 standalone: the LSE merge for plans with no K2 blocks at all (prefill plans whose causal
+// parts all ran in K1: every output row is a merge of its K1 partials).  Inside K2 such units
+// are latency chains (a warp merges its ~74 units one after another); here one warp merges one
+// (request, q-head) row with all its slots' loads in flight together, grid-stride over the rows
+// -> HBM-bound.  Same arithmetic as K2's finalize with an empty suffix state (online over the
+// slots in ascending order; the first slot sets the reference).
+namespace halo {
+namespace {
+
+template <int D>
+__global__ void __launch_bounds__(256) merge_only_kernel(const PlanDev p, int32_t hq, float *out, float *lse,
+                                                           int32_t layer) {
+    // K1 (the previous grid) wrote the partials: wait for it before reading them, and let the
+    // next layer's K1 start its prologue (it waits for this grid before writing partials)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.k1_done[layer & 3] = 0;  // K1 is complete: reset the hint
+    constexpr int C4 = D / 4;  // float4 chunks per row
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = (int64_t)p.nreq * hq, slot_stride = rows;
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+         row += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const int nslots = p.req_nslots[row / hq];
+        float M = -INFINITY, L = 0.f;
+        float4 acc[(C4 + 31) / 32];
+#pragma unroll
+        for (int k = 0; k < (C4 + 31) / 32; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        // up to kPre slots' loads issued together (one round trip), folded in slot order
+        constexpr int kPre = 4, KC = (C4 + 31) / 32;
+        float xs[kPre];
+        float4 vs[kPre][KC];
+#pragma unroll
+        for (int sl = 0; sl < kPre; ++sl)
+            if (sl < nslots) {
+                const int64_t r = sl * slot_stride + row;
+                xs[sl] = __ldcg(p.part_lse + r);
+#pragma unroll
+                for (int k = 0; k < KC; ++k)
+                    if (k * 32 + lane < C4) vs[sl][k] = __ldcg(reinterpret_cast<const float4 *>(p.part_o + r * D) + k * 32 + lane);
+            }
+        for (int sl = 0; sl < nslots; ++sl) {
+            const int64_t r = sl * slot_stride + row;
+            float x;
+            float4 v[KC];
+            if (sl < kPre) {
+#pragma unroll
+                for (int i = 0; i < kPre; ++i)
+                    if (i == sl) {
+                        x = xs[i];
+#pragma unroll
+                        for (int k = 0; k < KC; ++k) v[k] = vs[i][k];
+                    }
+            } else {
+                x = __ldcg(p.part_lse + r);
+#pragma unroll
+                for (int k = 0; k < KC; ++k)
+                    if (k * 32 + lane < C4) v[k] = __ldcg(reinterpret_cast<const float4 *>(p.part_o + r * D) + k * 32 + lane);
+            }
+            x *= kLog2e;
+            const float mn = fmaxf(M, x);
+            const float al = ptx::ex2(M - mn), w = ptx::ex2(x - mn);
+            L = L * al + w;
+            M = mn;
+#pragma unroll
+            for (int k = 0; k < (C4 + 31) / 32; ++k) {
+                acc[k].x = fmaf(w, v[k].x, acc[k].x * al);
+                acc[k].y = fmaf(w, v[k].y, acc[k].y * al);
+                acc[k].z = fmaf(w, v[k].z, acc[k].z * al);
+                acc[k].w = fmaf(w, v[k].w, acc[k].w * al);
+            }
+        }
+        const float inv = 1.f / L;
+#pragma unroll
+        for (int k = 0; k < (C4 + 31) / 32; ++k)
+            if (k * 32 + lane < C4)
+                reinterpret_cast<float4 *>(out + row * D)[k * 32 + lane] =
+                    make_float4(acc[k].x * inv, acc[k].y * inv, acc[k].z * inv, acc[k].w * inv);
+        if (lse != nullptr && lane == 0) lse[row] = (M + __log2f(L)) * kLn2;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_merge_only(const PlanDev &p, const PoolGeom &g, int layer, float *out, float *lse, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms * 16);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (g.d == 128) return cudaLaunchKernelEx(&cfg, merge_only_kernel<128>, p, g.hq, out, lse, (int32_t)layer);
+    if (g.d == 64) return cudaLaunchKernelEx(&cfg, merge_only_kernel<64>, p, g.hq, out, lse, (int32_t)layer);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace halo

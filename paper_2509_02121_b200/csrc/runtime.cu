@@ -808,6 +808,7 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
     k2_bytes = (double)pl->req_blk.size() * kBlockTok * hkv * D * 4 + (double)nreq * hq * D * 2 +
                (double)nreq * hq * (D + 1) * 4;
     for (int i = 0; i < nreq; ++i) k2_bytes += (double)pl->req_nslots[i] * hq * (D + 1) * 4;
+    if (pl->req_blk.empty()) k2_bytes -= (double)nreq * hq * D * 2;  // K3 alone reads no q
     // 12. K2 request order: longest block list first (LPT), stable
     pl->unit_req.resize(nreq);
     for (int i = 0; i < nreq; ++i) pl->unit_req[i] = i;
@@ -1266,8 +1267,14 @@ halo_status run_layer(halo_plan pl, int32_t layer, const void *q, float *out, fl
             dv.nchunks = dv.alt_nchunks;
             dv.dyn_first = dv.alt_nchunks;
         }
-        e = launch_suffix_decode(&p->tmap_k, &p->tmap_v, dv, p->geom, layer, q, out, lse, scale, s);
-        if (e != cudaSuccess) return fail(HALO_ECUDA, "suffix kernel launch: %s", cudaGetErrorString(e));
+        if (dv.nblocks == 0 && dv.nunits > 0 && dv.max_slots > 0) {
+            // no suffix blocks at all (prefill plans whose causal parts ran in K1): K3 alone
+            e = launch_merge_only(dv, p->geom, layer, out, lse, s);
+            if (e != cudaSuccess) return fail(HALO_ECUDA, "merge kernel launch: %s", cudaGetErrorString(e));
+        } else {
+            e = launch_suffix_decode(&p->tmap_k, &p->tmap_v, dv, p->geom, layer, q, out, lse, scale, s);
+            if (e != cudaSuccess) return fail(HALO_ECUDA, "suffix kernel launch: %s", cudaGetErrorString(e));
+        }
     }
     return HALO_OK;
 }

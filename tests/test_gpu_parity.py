@@ -430,15 +430,17 @@ def test_continuous_batching_requests_join_and_leave_between_steps():
     pool.destroy()
 
 
-@pytest.mark.parametrize("min_rows", [0, 1, 100000])
-def test_prefill_against_cached_prefixes_matches_oracle(min_rows):
+@pytest.mark.parametrize("min_rows,lo", [(0, 1), (1, 1), (100000, 1), (1, 16)])
+def test_prefill_against_cached_prefixes_matches_oracle(min_rows, lo):
     """halo_prefill_plan (NEXT-4): a burst of prompt tokens per request attends causally to
-    itself after the cached prefix path; every token row vs the oracle over its context."""
+    itself after the cached prefix path; every token row vs the oracle over its context.
+    lo=16: every prompt's causal part runs as K1 tiles, so the plan has no K2 blocks and the
+    merge runs as K3 alone (merge_only_kernel)."""
     wl = make_config("ragged", layers=2)
     ld = load(wl, DEV)
     rng = np.random.Generator(np.random.PCG64(3))
     sel = [i for i in range(wl.nreq) if i % 3 == 0]
-    nnew = [int(x) for x in rng.integers(1, 40, len(sel))]
+    nnew = [int(x) for x in rng.integers(lo, 40, len(sel))]
     # the prompt tokens of request r are the decode-step tokens 0..n-1 of the workload
     nkv = [wl.new_kv(s, "cuda") for s in range(max(nnew))]      # [L][R][Hkv][d] per step
     qs = [wl.q(s, "cuda") for s in range(max(nnew))]
@@ -448,6 +450,8 @@ def test_prefill_against_cached_prefixes_matches_oracle(min_rows):
         vs.append(torch.stack([nkv[s][1][:, r] for s in range(n)], dim=1))
     ld.pool.append([ld.req_ids[r] for r in sel], nnew, torch.cat(ks, 1).contiguous(), torch.cat(vs, 1).contiguous())
     plan = ld.pool.prefill_plan([ld.req_ids[r] for r in sel], nnew, opts(min_rows=min_rows))
+    if lo == 16 and wl.hq // wl.hkv >= 4:
+        assert len(plan.export("req_blk")) == 0  # K3 alone
     rows = sum(nnew)
     qrows = torch.cat([torch.stack([qs[s][:, r] for s in range(n)], dim=1)
                        for r, n in zip(sel, nnew)], 1).contiguous()      # [L][rows][Hq][d]

@@ -2066,6 +2066,7 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
             HALO_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking));
             HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_step, cudaEventDisableTiming));
             HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_copied, cudaEventDisableTiming));
+            for (int b = 0; b < 2; ++b) HALO_CUDA(cudaEventCreateWithFlags(&pl->ev_used[b], cudaEventDisableTiming));
         }
         while ((int)pl->ev_in.size() < L) {
             cudaEvent_t a, b;
@@ -2074,8 +2075,8 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
             pl->ev_in.push_back(a);
             pl->ev_out.push_back(b);
         }
-        if (kv_host && (st = grow(&pl->kv_stage, &pl->kv_stage_cap, 2 * kv_layer * L * 2)) != HALO_OK) return st;
-        if (q_host && (st = grow(&pl->q_stage, &pl->q_stage_cap, q_layer * L * 2)) != HALO_OK) return st;
+        if (kv_host && (st = grow(&pl->kv_stage, &pl->kv_stage_cap, 2 * (2 * kv_layer * L * 2))) != HALO_OK) return st;
+        if (q_host && (st = grow(&pl->q_stage, &pl->q_stage_cap, 2 * (q_layer * L * 2))) != HALO_OK) return st;
         if (o_host && (st = grow((void **)&pl->o_stage, &pl->o_stage_cap, q_layer * L * 4)) != HALO_OK) return st;
         if (l_host && (st = grow((void **)&pl->l_stage, &pl->l_stage_cap, rows * L * 4)) != HALO_OK) return st;
         if ((st = grow((void **)&pl->slot_stage, &pl->slot_stage_cap, w.slots.size() * 8)) != HALO_OK) return st;
@@ -2100,13 +2101,19 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
     //    (out, lse) on the d2h stream in chunks of kD2HLayers layers.  Chunk sizes measured on
     //    B200 + PCIe host (tools/e2e_pipe_probe.py, C1): per-layer copies 4.0 ms/step, H2D x4 +
     //    D2H x2 3.07 ms/step (both directions share ~89 GB/s; small D2H chunks start the
-    //    output stream early, larger H2D chunks cut the per-copy overhead).  The staging
-    //    buffers are reused step to step: the copy streams first wait for `stream`.
+    //    output stream early, larger H2D chunks cut the per-copy overhead).  The input staging
+    //    is double-buffered: this step's uploads wait only for the compute of the step that
+    //    last read the same buffer (two calls ago), so they overlap the previous step's tail
+    //    (its last layers and downloads) -- the host link then stays busy in both directions.
     constexpr int kH2DLayers = 4, kD2HLayers = 2;
+    const int par = pl->e2e_par;
+    pl->e2e_par ^= 1;
     HALO_CUDA(cudaEventRecord(pl->ev_step, s));
-    HALO_CUDA(cudaStreamWaitEvent(pl->h2d, pl->ev_step, 0));
+    if (pl->ev_used_rec[par]) HALO_CUDA(cudaStreamWaitEvent(pl->h2d, pl->ev_used[par], 0));
     HALO_CUDA(cudaStreamWaitEvent(pl->d2h, pl->ev_step, 0));
-    uint16_t *sk = static_cast<uint16_t *>(pl->kv_stage), *sv = sk ? sk + kv_layer * L : nullptr;
+    uint16_t *sk = kv_host ? static_cast<uint16_t *>(pl->kv_stage) + par * (2 * kv_layer * L) : nullptr;
+    uint16_t *sv = sk ? sk + kv_layer * L : nullptr;
+    uint16_t *sq = q_host ? static_cast<uint16_t *>(pl->q_stage) + par * (q_layer * L) : nullptr;
     for (int l = 0; l < L; l += kH2DLayers) {
         const int n = std::min(kH2DLayers, L - l);
         if (kv_host) {
@@ -2116,14 +2123,13 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
                                       kv_layer * 2 * n, cudaMemcpyHostToDevice, pl->h2d));
         }
         if (q_host)
-            HALO_CUDA(cudaMemcpyAsync(static_cast<uint16_t *>(pl->q_stage) + q_layer * l,
-                                      static_cast<const uint16_t *>(q) + q_layer * l, q_layer * 2 * n,
-                                      cudaMemcpyHostToDevice, pl->h2d));
+            HALO_CUDA(cudaMemcpyAsync(sq + q_layer * l, static_cast<const uint16_t *>(q) + q_layer * l,
+                                      q_layer * 2 * n, cudaMemcpyHostToDevice, pl->h2d));
         HALO_CUDA(cudaEventRecord(pl->ev_in[l], pl->h2d));
     }
     const uint16_t *dk = kv_host ? sk : static_cast<const uint16_t *>(k_new);
     const uint16_t *dv = kv_host ? sv : static_cast<const uint16_t *>(v_new);
-    const uint16_t *dq = q_host ? static_cast<const uint16_t *>(pl->q_stage) : static_cast<const uint16_t *>(q);
+    const uint16_t *dq = q_host ? sq : static_cast<const uint16_t *>(q);
     float *dout = o_host ? pl->o_stage : out;
     float *dlse = l_host ? pl->l_stage : lse;
     if (!kv_host) {  // device-resident new K/V: one K5 launch appends every layer
@@ -2152,6 +2158,9 @@ halo_status halo_decode_step(halo_pool p, int32_t nreq, const int64_t *reqs, con
                                           pl->d2h));
         }
     }
+    // the compute of this step has read the input staging buffer `par`
+    HALO_CUDA(cudaEventRecord(pl->ev_used[par], s));
+    pl->ev_used_rec[par] = true;
     // the step is complete in `stream` order once the last download has landed
     HALO_CUDA(cudaEventRecord(pl->ev_copied, pl->d2h));
     HALO_CUDA(cudaStreamWaitEvent(s, pl->ev_copied, 0));
@@ -2210,6 +2219,8 @@ halo_status halo_plan_destroy(halo_plan pl) {
         for (cudaEvent_t e : pl->ev_out) cudaEventDestroy(e);
         if (pl->ev_step) cudaEventDestroy(pl->ev_step);
         if (pl->ev_copied) cudaEventDestroy(pl->ev_copied);
+        for (int b = 0; b < 2; ++b)
+            if (pl->ev_used[b]) cudaEventDestroy(pl->ev_used[b]);
         if (pl->h2d) cudaStreamDestroy(pl->h2d);
         if (pl->d2h) cudaStreamDestroy(pl->d2h);
     }

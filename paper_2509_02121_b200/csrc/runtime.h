@@ -194,6 +194,11 @@ struct halo_plan_s {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_out;
     cudaEvent_t ev_step = nullptr, ev_copied = nullptr;
+    // halo_decode_step's input staging is double-buffered (parity e2e_par): ev_used[b] marks
+    // the end of the compute that last read buffer b, which the next upload into b waits for
+    cudaEvent_t ev_used[2] = {nullptr, nullptr};
+    bool ev_used_rec[2] = {false, false};
+    int e2e_par = 0;
     void *kv_stage = nullptr;
     size_t kv_stage_cap = 0;
     int32_t *slot_stage = nullptr;

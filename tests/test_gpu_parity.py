@@ -605,3 +605,29 @@ def test_stream_k_pieces_beside_a_long_k1_park_and_merge():
     torch.cuda.synchronize()
     assert np.array_equal(o2.cpu().numpy(), out[1]) and np.array_equal(l2.cpu().numpy(), lse[1])
     cleanup(ld, plan)
+
+
+def test_decode_step_host_buffers_back_to_back_steps_match_oracle():
+    """halo_decode_step with pinned HOST inputs and outputs, four steps issued back to back
+    with no synchronisation in between (the input staging is double-buffered: a step's uploads
+    overlap the previous step's last layers and downloads); every step's output vs the oracle."""
+    wl = make_config("fanout", layers=3, nreq=40, prefix=150, suffix=20)
+    ld = load(wl, DEV)
+    L = wl.layers
+    steps = 4
+    ins, outs = [], []
+    for step in range(steps):
+        nk, nv = wl.new_kv(step, "cpu")
+        q = wl.q(step, "cpu")
+        ins.append((nk.pin_memory(), nv.pin_memory(), q.pin_memory()))
+        outs.append(torch.empty((L, wl.nreq, wl.hq, wl.d)).pin_memory())
+    plan = None
+    for step in range(steps):
+        nk, nv, q = ins[step]
+        plan = ld.pool.decode_step(ld.req_ids, nk, nv, q, outs[step], reuse=plan)
+    torch.cuda.synchronize()
+    for step in range(steps):
+        for layer in range(L):
+            ro, _ = oracle.decode_reference(wl, layer, steps=step + 1)
+            assert np.abs(outs[step][layer].numpy() - ro).max() <= OUT_TOL, (step, layer)
+    cleanup(ld, plan)

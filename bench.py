@@ -745,6 +745,8 @@ def measure_prefill(halo, dev, torch, steps=10, prompt=64, layers=4):
     k1 = sum(e[0].elapsed_time(e[1]) for e in ev) / n
     k2 = sum(e[1].elapsed_time(e[2]) for e in ev) / n
     k2r, k1r = kernel_rooflines(info, k1, k2)
+    if len(plan.export("req_blk")) == 0:  # every causal part in K1: the merge runs as K3 alone
+        k2r["kernel"] = "merge_only_kernel (K3 alone: no suffix blocks in the plan)"
     plan.destroy()
     pool.destroy()
     return {"what": f"prefill of a {prompt}-token prompt for each of {R} requests against the cached "

@@ -31,7 +31,7 @@ class PlanOptions(C.Structure):
     _fields_ = [("min_tensor_rows", _i32), ("force_splits", _i32), ("max_splits", _i32),
                 ("k2_chunk_blocks", _i32), ("k2_shape", _i32), ("k2_sms", _i32),
                 ("k1_sm_frac", C.c_float), ("k2_early_weight", C.c_float),
-                ("k2_tail_pct", _i32), ("reserved", _i32)]
+                ("k2_tail_pct", _i32), ("k2_whole_units", _i32)]
 
 
 class PlanInfo(C.Structure):

@@ -888,7 +888,9 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         };
         std::vector<int64_t> cuts;
         bool bal = false;
-        const bool few_units = U > Ww && U <= 3 * Wn;  // 1-3 whole units per narrow warp
+        // 1-3 whole units per narrow warp (opt-in, halo_plan_options.k2_whole_units: this
+        // schedule's run-to-run spread is large, profiles/k2_alone_variance_r02.txt)
+        const bool few_units = pl->opt.k2_whole_units > 0 && U > Ww && U <= 3 * Wn;
         if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
             cuts.assign(1, 0);
             for (int64_t x = pl->opt.k2_chunk_blocks; x < Itot; x += pl->opt.k2_chunk_blocks) push_cut(cuts, x);
@@ -989,13 +991,14 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
             const int32_t b0 = pl->unit_boff[uu], b1 = pl->unit_boff[uu + 1];
             const int32_t rb = pl->req_blk_off[req];
             for (int32_t x = b0; x < b1; ++x) {
-                const uint32_t e = pl->req_blk[rb + (x - b0)];
+                const int32_t j = x - b0;
+                const uint32_t e = pl->req_blk[rb + j];
                 const uint32_t slab = (e & kBlkMask) * (uint32_t)hkv + (uint32_t)head;
                 pl->k2_ent[2 * (size_t)x] = slab | (e & ~kBlkMask) | (x == b0 ? 0x80000000u : 0u);
                 // bit 31: a block of a folded prefix node, read by every request under the node:
                 // K2 streams it with the default L2 policy instead of evict_first
                 pl->k2_ent[2 * (size_t)x + 1] = (uint32_t)(req * hkv + head) |
-                                                ((x - b0) < req_fold_blk[req] ? 0x80000000u : 0u);
+                                                (j < req_fold_blk[req] ? 0x80000000u : 0u);
             }
             int32_t *um = &pl->unit_meta[(size_t)uu * 8];
             um[0] = b0; um[1] = b1; um[2] = req; um[3] = head;

@@ -245,11 +245,15 @@ def time_steps(step, L, steps, warmup, world, dev, torch, dist, sample_clocks=Fa
     Returns (pass-1 ms, pass-2 ms of the steps' layer spans, pass-2 K1 ms, pass-2 K2 ms,
     clock sampler)."""
     stream = torch.cuda.current_stream()
-    for _ in range(warmup):
-        step()
-    torch.cuda.synchronize()
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)]
            for _ in range(steps)]
+    for w in range(warmup):
+        # the last warm-up step runs the breakdown pass's launch sequence (K2 launched alone
+        # uses the plan's K2-alone schedule, possibly another kernel instantiation): with lazy
+        # module loading its first launch would otherwise load the kernel inside a timed
+        # event interval (a 10-80 ms stall once per process)
+        step(evs[0] if w == warmup - 1 else None)
+    torch.cuda.synchronize()
     t = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     clk = ClockSampler(dev) if sample_clocks else None
     if clk:

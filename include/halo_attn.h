@@ -171,11 +171,10 @@ typedef struct {
     int32_t k2_tail_pct;     /* > 0: K2's last k2_tail_pct % of blocks are cut into small
                                 pieces that warps claim dynamically once their static share
                                 is done; <= 0: off (default: measured slower at C1)        */
-    int32_t k2_whole_units;  /* > 0: with few units per warp and no K1 beside it, K2 runs
-                                whole units over the narrow shape (no stream-K pieces;
-                                C1 K2 alone 0.83 of HBM in most runs but 0.45-0.77 in about
-                                a third of the processes); <= 0: the wide shape with pieces
-                                (default: 0.79-0.80, stable)                               */
+    int32_t k2_whole_units;  /* >= 0 (default): with few units per warp and no K1 beside
+                                it, K2 runs whole units over the narrow shape (no stream-K
+                                pieces; C1 K2 alone 0.83 of HBM); < 0: the wide shape with
+                                pieces (0.78-0.80)                                          */
 } halo_plan_options;
 
 /* Build (or rebuild in place, when *inout != NULL) the plan of one decode step for the

@@ -888,9 +888,8 @@ halo_status build_plan(halo_plan pl, int32_t nreq, const int64_t *reqs,
         };
         std::vector<int64_t> cuts;
         bool bal = false;
-        // 1-3 whole units per narrow warp (opt-in, halo_plan_options.k2_whole_units: this
-        // schedule's run-to-run spread is large, profiles/k2_alone_variance_r02.txt)
-        const bool few_units = pl->opt.k2_whole_units > 0 && U > Ww && U <= 3 * Wn;
+        // 1-3 whole units per narrow warp (halo_plan_options.k2_whole_units < 0: off)
+        const bool few_units = pl->opt.k2_whole_units >= 0 && U > Ww && U <= 3 * Wn;
         if (pl->opt.k2_chunk_blocks > 0) {  // fixed-size chunks (tests)
             cuts.assign(1, 0);
             for (int64_t x = pl->opt.k2_chunk_blocks; x < Itot; x += pl->opt.k2_chunk_blocks) push_cut(cuts, x);

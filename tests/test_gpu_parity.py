@@ -564,12 +564,12 @@ def test_plan_is_stale_after_blocks_are_given_back():
     cleanup(ld, plan)
 
 
-@pytest.mark.parametrize("whole", [0, 1])
+@pytest.mark.parametrize("whole", [0, -1])
 def test_k2_alone_uses_the_equal_share_schedule_and_matches_oracle(whole):
     """With the K1/K2 co-schedule on (C1 shape), K2 launched by itself after K1
-    (halo_decode_run_stages K1 then K2) runs the plan's K2-alone schedule (equal shares; with
-    k2_whole_units, whole units over the narrow shape, no stream-K pieces), K1+K2 launched
-    together the weighted wide one with pieces; both match the oracle."""
+    (halo_decode_run_stages K1 then K2) runs the plan's K2-alone schedule (C1: whole units over
+    the narrow shape, no stream-K pieces; k2_whole_units = -1: wide, equal shares), K1+K2
+    launched together the weighted wide one with pieces; both match the oracle."""
     wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=255)
     ld = load(wl, DEV)
     append_step(ld, wl, 0, DEV)

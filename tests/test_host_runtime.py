@@ -351,23 +351,23 @@ def test_single_wave_k1_rule_lowers_splits_and_weights_early_k2_warps():
 
 
 def test_k2_launch_shape_whole_units_when_few_units_per_warp():
-    """Planner 12b (opt-in, k2_whole_units): with few (request, kv head) units per warp and no
-    K1 beside K2 (here every prefix node folded into K2), whole units over the narrow shape
-    (7 warps x 4 stages per SM) replace stream-K pieces -- C1 has 2048 units for 1776 wide
-    warps, so nearly every unit would be cut in two (K2, "Unit ends").  Default: the
-    wide shape with pieces (stable run to run); beside a co-scheduled K1 always wide."""
+    """Planner 12b: with few (request, kv head) units per warp and no K1 beside K2 (here every
+    prefix node folded into K2), whole units over the narrow shape (7 warps x 4 stages per SM)
+    replace stream-K pieces -- C1 has 2048 units for 1776 wide warps, so nearly every unit
+    would be cut in two (K2, "Unit ends"); k2_whole_units < 0 opts out.  Beside a
+    co-scheduled K1 always wide."""
     wl = make_config("fanout", layers=1, nreq=256, prefix=2048, suffix=255)
     p, ld, pl = plan_of(wl)  # K1 tiles + co-schedule: wide
     info = pl.info()
     assert info["k1_tiles"] > 0 and info["k2_warps"] == 12
     pl.destroy(); p.destroy()
-    p, ld, pl = plan_of(wl, min_rows=1 << 20)  # everything folded: K2 alone, default: wide
-    assert pl.info()["k2_warps"] == 12
-    pl.destroy(); p.destroy()
-    p, ld, pl = plan_of(wl, min_rows=1 << 20, whole_units=1)  # opt-in: whole units, narrow
+    p, ld, pl = plan_of(wl, min_rows=1 << 20)  # everything folded: K2 alone, whole units
     info = pl.info()
     assert info["k1_tiles"] == 0 and info["k2_warps"] == 7
     assert (pl.export("unit_nseg") == 1).all()  # whole units: no stream-K pieces
+    pl.destroy(); p.destroy()
+    p, ld, pl = plan_of(wl, min_rows=1 << 20, whole_units=-1)  # opted out: wide with pieces
+    assert pl.info()["k2_warps"] == 12
     pl.destroy(); p.destroy()
     # many units per warp (C2: 8192 units): the wide shape
     wl = make_config("tree", layers=1)

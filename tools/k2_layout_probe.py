@@ -25,7 +25,10 @@ def main():
         ld = load(wl, 0, capacity=blocks_needed(wl, steps=2, slack=4096))
         nk, nv = wl.new_kv(0, "cuda:0")
         ld.pool.append(ld.req_ids, [1] * wl.nreq, nk, nv)
-        plan = ld.pool.plan(ld.req_ids)
+        popt = halo.PlanOptions(0, 0, 0, 0)
+        popt.k2_whole_units = int(os.environ.get("WHOLE_UNITS", "1"))
+        plan = ld.pool.plan(ld.req_ids, popt)
+        ones = [1] * wl.nreq
         res = []
         for rep in range(int(os.environ.get("REPS", "3"))):
             if os.environ.get("HEADLINE"):  # the bench's headline pass first (K1 -> K2 under PDL)
@@ -33,6 +36,10 @@ def main():
                     for l in range(L):
                         plan.run(l, q[l], out[l])
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+            if os.environ.get("STEP"):  # the bench's step: roll back, re-append, re-plan
+                ld.pool.truncate(ld.req_ids, ones)
+                ld.pool.append(ld.req_ids, ones, nk, nv)
+                ld.pool.plan(ld.req_ids, popt, reuse=plan)
             torch.cuda._sleep(4_000_000)
             for l in range(L):
                 plan.run_stages(l, 1, q[l], out[l])

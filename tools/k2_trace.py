@@ -42,6 +42,7 @@ def main():
     opt = PlanOptions(0, 0, int(os.environ.get("SPLITS", "0")), 0)
     opt.k2_early_weight = float(os.environ.get("EARLY_W", "0"))
     opt.k1_sm_frac = float(os.environ.get("K1_SM_FRAC", "0"))
+    opt.k2_whole_units = int(os.environ.get("WHOLE_UNITS", "0"))
     plan = ld.pool.plan(ld.req_ids, opt)
     info = plan.info()
     q = wl.q(0, "cuda:0")

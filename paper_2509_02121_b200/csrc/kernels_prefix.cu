@@ -73,11 +73,10 @@ extern "C" int halo_debug_k1_trace(void *buf) {
 #endif
 
 #ifndef HALO_K1_PINGPONG
-// MUFU ping-pong between the sub-tiles' exp passes: 1 strict A/B alternation, 2 B after A only,
-// 0 none (default: C3 0.55 -> 0.56, C2 root 0.450 -> 0.457; profiles/k1_pingpong_ab_r02.txt)
+// MUFU ping-pong between the sub-tiles' exp passes: 1 = strict A/B alternation, 0 = none
+// (default: C3 0.55 -> 0.56, C2 root 0.450 -> 0.457; profiles/k1_pingpong_ab_r02.txt)
 #define HALO_K1_PINGPONG 0
 #endif
-
 
 namespace halo {
 namespace {
@@ -499,7 +498,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             if (hasB && HALO_K1_PINGPONG) {
                 // per SMSP: warp w of A pairs with warp w + 4 of B (same scheduler, same MUFU)
                 if (x == 1) ptx::mbar_wait(&bar[EXP_DONE + wq], n & 1);
-                else if (n >= 1 && HALO_K1_PINGPONG == 1) ptx::mbar_wait(&bar[EXP_DONE + 4 + wq], (n - 1) & 1);
+                else if (n >= 1) ptx::mbar_wait(&bar[EXP_DONE + 4 + wq], (n - 1) & 1);
             }
             if (threadIdx.x == 0) K1_TRACE(7, n);
             const float2 c2v = make_float2(c2, c2), nm = make_float2(-m_ref, -m_ref);
@@ -528,8 +527,7 @@ prefix_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constan
             }
             const float2 a01 = ptx::fadd2(acc[0], acc[1]), a23 = ptx::fadd2(acc[2], acc[3]);
             l += (a01.x + a01.y) + (a23.x + a23.y);
-            if (hasB && (HALO_K1_PINGPONG == 1 || (HALO_K1_PINGPONG == 2 && x == 0)))
-                ptx::mbar_arrive(&bar[EXP_DONE + 4 * x + wq]);
+            if (hasB && HALO_K1_PINGPONG) ptx::mbar_arrive(&bar[EXP_DONE + 4 * x + wq]);
             if (threadIdx.x == 0) K1_TRACE_DEP(11, n, l);
             if (threadIdx.x == 128) K1_TRACE_DEP(13, n, l);
             if (n == 0) {  // the tile's V scale (set by the converters before their first arrive)

@@ -41,6 +41,13 @@ TIMING_NOTE = ("CUDA events on the launching stream around every launch of the k
                "over the K-step breakdown pass (same workload, right after the headline pass)")
 
 
+def gate(torch, cycles=6_000_000):
+    """Hold the stream for ~3 ms (a spin kernel) while the host enqueues a timed sequence, so no
+    event interval holds host enqueue latency; a no-op where torch has no spin kernel."""
+    if hasattr(torch.cuda, "_sleep"):
+        torch.cuda._sleep(cycles)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -220,7 +227,7 @@ def setup_workload(halo, wl, dev, torch):
             # while the host enqueues the step's 32 x (event, K1, event, K2, event), so no
             # interval between two events contains host enqueue latency
             if os.environ.get('HALO_BENCH_GATE', '1') == '1':
-                torch.cuda._sleep(6_000_000)
+                gate(torch)
         for l in range(L):
             if evs is None:                       # headline pass: K1 -> K2 back to back (PDL)
                 plan.run(l, q[l], out[l], lse[l])
@@ -581,7 +588,7 @@ def main():
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
             for rep in range(4):
                 if rep == 3:
-                    torch.cuda._sleep(6_000_000)  # the timed layers enqueued behind a spin kernel
+                    gate(torch)  # the timed layers enqueued behind a spin kernel
                 for l in range(L):
                     ep.run_stages(l, 1, q[l], out[l], lse[l])
                     if rep == 3:

@@ -10,7 +10,7 @@ namespace halo {
 constexpr int kBlockTok = 16;       // tokens per KV block
 constexpr int kK1Rows = 256;        // K1 tile rows (two UMMA M=128 sub-tiles)
 constexpr int kK1Tok = 128;         // K1 tokens per n-tile (UMMA N of S, K of P.V)
-constexpr int kK1MaxTileTok = 3072;  // max token range of one K1 tile (split-N above this; bounded by smem)
+constexpr int kK1MaxTileTok = 4096;  // max token range of one K1 tile (split-N above this; bounded by smem)
 // K2 launch shapes (one CTA per SM): "wide" = 12 warps x 2 ring stages (many units per warp:
 // best latency hiding), "narrow" = 7 warps x 4 stages (chosen by the planner when units are
 // few per warp and whole units divide evenly over 7 warps per SM: no stream-K pieces).

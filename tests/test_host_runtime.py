@@ -273,6 +273,10 @@ def test_prefill_plan_rows_are_causal_virtual_requests():
     assert sorted(int(t[4]) for t in causal) == [20, 20, 40, 40]   # token range = visible max
     nsl = pl.export("req_nslots")
     assert list(nsl[:20]) == [2] * 20 and list(nsl[20:]) == [1] * 33   # prefix + causal slots
+    # no K2 blocks: the merge runs as K3 alone, whose algorithmic bytes are the partial rows read
+    # plus out / lse written (no q): sum_r slots_r * Hq * (d+1) * 4 + R * Hq * (d+1) * 4
+    d, hq, R = 128, 8, 53
+    assert info["k2_bytes"] == (int(nsl.sum()) + R) * hq * (d + 1) * 4
     pl.destroy()
     for bad in ([0, 1], [21, 1], [1, 41]):
         with pytest.raises(halo.HaloError) as e:

@@ -2003,6 +2003,12 @@ halo_status halo_decode_layers(halo_plan pl, int32_t nlayers, const void *q, flo
                        dlse ? dlse + rows * l : nullptr, scale, s);
         if (st != HALO_OK) return st;
     }
+    if (q_host && pl->ev_used[0]) {
+        // the input staging's buffer 0 was read by these layers: halo_decode_step's next upload
+        // into it (double-buffered staging) waits for them
+        HALO_CUDA(cudaEventRecord(pl->ev_used[0], s));
+        pl->ev_used_rec[0] = true;
+    }
     if (o_host) HALO_CUDA(cudaMemcpyAsync(out, dout, o_layer * nlayers * 4, cudaMemcpyDeviceToHost, s));
     if (l_host) HALO_CUDA(cudaMemcpyAsync(lse, dlse, rows * nlayers * 4, cudaMemcpyDeviceToHost, s));
     return HALO_OK;

@@ -634,3 +634,31 @@ def test_decode_step_host_buffers_back_to_back_steps_match_oracle():
             ro, _ = oracle.decode_reference(wl, layer, steps=step + 1)
             assert np.abs(outs[step][layer].numpy() - ro).max() <= OUT_TOL, (step, layer)
     cleanup(ld, plan)
+
+
+def test_decode_step_and_decode_layers_share_staging_without_races():
+    """A plan used by halo_decode_step (double-buffered input staging) and halo_decode_layers
+    (which stages host q in buffer 0) in alternation, every call with pinned host buffers and
+    no synchronisation in between: each call's outputs equal the device-buffer reference."""
+    wl = make_config("fanout", layers=2, nreq=32, prefix=120, suffix=12)
+    ld = load(wl, DEV)
+    L = wl.layers
+    plan = None
+    ins, outs = [], []
+    for step in range(3):
+        nk, nv = wl.new_kv(step, "cpu")
+        q = wl.q(step, "cpu")
+        ins.append((nk.pin_memory(), nv.pin_memory(), q.pin_memory()))
+        outs.append((torch.empty((L, wl.nreq, wl.hq, wl.d)).pin_memory(),
+                     torch.empty((L, wl.nreq, wl.hq, wl.d)).pin_memory()))
+    for step in range(3):
+        nk, nv, q = ins[step]
+        plan = ld.pool.decode_step(ld.req_ids, nk, nv, q, outs[step][0], reuse=plan)
+        plan.run_layers(L, q, outs[step][1])  # the same step's layers again through decode_layers
+    torch.cuda.synchronize()
+    for step in range(3):
+        assert torch.equal(outs[step][0], outs[step][1]), step
+        for layer in range(L):
+            ro, _ = oracle.decode_reference(wl, layer, steps=step + 1)
+            assert np.abs(outs[step][0][layer].numpy() - ro).max() <= OUT_TOL, (step, layer)
+    cleanup(ld, plan)

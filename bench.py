@@ -562,6 +562,13 @@ def main():
     k2_launch_ms = k2_ms / (args.steps * L)
     k1_launch_ms = k1_ms / (args.steps * L)
     k2_roof, k1_roof = kernel_rooflines(info, k1_launch_ms, k2_launch_ms)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    if k1_roof.get("frac") and 0 < info["k1_tiles"] < nsm:
+        # C1's K1 is planned as one partial wave (the co-schedule leaves the other SMs to K2):
+        # the rate per SM it occupies, for comparison with the multi-wave configs
+        k1_roof["note"] = (f"single partial wave of {info['k1_tiles']} CTAs on {nsm} SMs by design "
+                           f"(K2 streams on the rest); frac_per_occupied_sm = frac x {nsm}/{info['k1_tiles']}")
+        k1_roof["frac_per_occupied_sm"] = k1_roof["frac"] * nsm / info["k1_tiles"]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):

@@ -109,6 +109,14 @@ __global__ void kv_scatter_kernel(int4 *__restrict__ pk, int4 *__restrict__ pv,
                 const int32_t blk = i < g.n ? (slots[i] >> 4) : -1;
                 const uint32_t m = blk >= 0 ? absmax8(vv[u]) : 0u;
                 const uint32_t act = __activemask();
+                if (inner % 32 == 0 && act == 0xffffffffu) {
+                    // a whole warp lies in one token row (one block): one reduction, one atomic
+                    const uint32_t red = __reduce_max_sync(act, m);
+                    if (blk >= 0 && (threadIdx.x & 31) == 0)
+                        atomicMax(reinterpret_cast<unsigned long long *>(vmax + (int64_t)layer * cap + blk),
+                                  (unsigned long long)vmax_entry(tags[i], red));
+                    continue;
+                }
                 const uint32_t grp = __match_any_sync(act, blk);
                 const uint32_t red = __reduce_max_sync(grp, m);
                 if (blk >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1)
